@@ -1,0 +1,146 @@
+/*
+ * mm.h -- C ABI of the B200 (sm_100a) FP64 matrix-multiplication library implementing the
+ * methods of Hedtke, "Methods of Matrix Multiplication" (arXiv 1106.1347).
+ *
+ * Citations "P:L" refer to /root/reference/PAPER.md line L.
+ *
+ * Problem statement: "A denotes a N x P matrix and B denotes a P x M matrix with
+ * entries of type double".  Every entry point below computes C = A B, C being N x M.
+ *
+ * Conventions shared by every function:
+ *  - Layout: A, B, C are DENSE ROW-MAJOR float64 buffers with leading dimensions P, M and M
+ *    (A[i][k] = A[i*P + k]).  All pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors) on the current CUDA device unless a parameter says "host".
+ *  - Ownership: the caller owns A, B, C and the workspace; the library never allocates or
+ *    frees on these paths and keeps no reference after the call returns.  The library's
+ *    only persistent state is per-process kernel attributes.
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered and return after enqueue (asynchronous), except where a host output
+ *    pointer is given (documented per function), which synchronises the stream.
+ *  - Errors: return MM_OK (0) or a negative mm_status.  MM_ERR_ARG: NULL pointer,
+ *    N, P or M < 1, or an element count overflowing int64.  MM_ERR_ALIAS: C overlaps A or B.
+ *    MM_ERR_WORKSPACE: ws_bytes < mm_workspace_size(...).  MM_ERR_UNSUPPORTED: the current
+ *    device is not compute capability 10.0 (sm_100a) -- there is no fallback of any kind.
+ *    MM_ERR_CUDA: a launch or CUDA runtime call failed (device faults surface at the
+ *    caller's next synchronisation).  On error nothing is enqueued unless MM_ERR_CUDA.
+ *  - Arithmetic is IEEE binary64 round-to-nearest-even throughout; DESIGN.md lists, per
+ *    method, which oracle function each kernel reproduces bit for bit.
+ */
+#ifndef MM_B200_H
+#define MM_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MM_OK = 0,
+  MM_ERR_ARG = -1,
+  MM_ERR_ALIAS = -2,
+  MM_ERR_WORKSPACE = -3,
+  MM_ERR_CUDA = -4,
+  MM_ERR_UNSUPPORTED = -6
+} mm_status;
+
+/* method ids for mm_workspace_size / mm_gemm */
+typedef enum {
+  MM_NAIVE = 0,            /* P:102-106 NaivStandard (also NaivOnArray, unrolled variants) */
+  MM_KAHAN = 1,            /* P:111-134 NaivKahan */
+  MM_WINOGRAD = 2,         /* P:186-195 WinogradOriginal */
+  MM_WINOGRAD_SCALED = 3,  /* P:197-217 WinogradScaled */
+  MM_STRASSEN = 4,         /* P:251-291 StrassenNaiv */
+  MM_STRASSEN_WINOGRAD = 5 /* P:294-315 StrassenWinograd */
+} mm_method;
+
+/* Library version string and a human-readable message for a status code. */
+const char* mm_version(void);
+const char* mm_status_string(int status);
+
+/*
+ * mm_naive -- (AB)_ij = sum_k A_ik B_kj (NaivStandard P:105-106).
+ * FP64 tensor-core (DMMA) GEMM; k is walked in increasing order as one fused
+ * multiply-add chain per entry (reading R2).  No workspace.
+ */
+int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream);
+
+/*
+ * mm_kahan -- NaivKahan: each entry is the compensated sum of the products
+ * A_ik B_kj, k increasing, with the update of P:122-132
+ * (err = err + x; t = sum + err; err = (sum - t) + err; sum = t), result `sum`.
+ * Separately rounded FP64 operations, no contraction.  No workspace.
+ */
+int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream);
+
+/*
+ * mm_winograd -- WinogradOriginal: y_i = sum_j A_{i,2j-1}A_{i,2j},
+ * z_k = sum_j B_{2j-1,k}B_{2j,k}, C_ik = (sum_j (A_{i,2j-1}+B_{2j,k})(A_{i,2j}+B_{2j-1,k}) - y_i) - z_k,
+ * plus A_{i,P}B_{P,k} when P is odd.  Sums in increasing j, separately rounded.
+ * workspace: device buffer of at least mm_workspace_size(MM_WINOGRAD, N, P, M, 0) bytes
+ * (holds y and z), 256-byte aligned.
+ */
+int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * mm_winograd_scaled -- WinogradScaled: lambda is the integer with
+ * 1/2 <= 2^lambda ||A||_inf / (2^-lambda ||B||_inf) <= 2 (tie -> larger |lambda|,
+ * zero norm -> 0), then WinogradOriginal on (2^lambda A, 2^-lambda B); C is not rescaled
+ * (P:216).  Norms and lambda are computed on the device (no host sync).
+ * workspace: >= mm_workspace_size(MM_WINOGRAD_SCALED, N, P, M, 0) bytes.
+ * lambda_out: HOST int32 pointer or NULL; when non-NULL the call synchronises `stream`
+ * and stores lambda there.
+ */
+int mm_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                       void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
+
+/*
+ * mm_strassen / mm_strassen_winograd -- StrassenNaiv (H_1..H_7 of P:271-277,
+ * C blocks of P:279-282) and StrassenWinograd.  `levels` >= 0 recursion levels
+ * with each dimension zero-padded to the next multiple of 2^(levels+1) (DESIGN.md reading
+ * R10; mm_strassen_plan reports the padded dims); levels == -1 selects the paper's plan
+ * (X = max{N,P,M}, k = floor(log2 X) - 4 clamped at 0, m = floor(X 2^-k) + 1,
+ * embed in Y x Y with Y = m 2^k, k levels).  The base case alpha_{m,0} is the DMMA GEMM of
+ * mm_naive, batched over all 7^levels products.  levels in [-1, 8].
+ * workspace: >= mm_workspace_size(MM_STRASSEN[_WINOGRAD], N, P, M, levels) bytes.
+ */
+int mm_strassen(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, int32_t levels,
+                void* workspace, size_t ws_bytes, void* stream);
+int mm_strassen_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                         int32_t levels, void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * mm_strassen_plan -- the recursion depth and padded dimensions mm_strassen uses for
+ * (N, P, M, levels): HOST output pointers.  Returns MM_ERR_ARG on bad sizes/levels.
+ */
+int mm_strassen_plan(int64_t N, int64_t P, int64_t M, int32_t levels, int32_t* depth_out, int64_t* Np_out,
+                     int64_t* Pp_out, int64_t* Mp_out);
+
+/* Workspace bytes the given method needs (0 for MM_NAIVE and MM_KAHAN); 0 on bad arguments. */
+size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels);
+
+/*
+ * mm_gemm -- dispatch by mm_method id (levels only used by the Strassen methods,
+ * lambda_out only by MM_WINOGRAD_SCALED; both may be 0/NULL otherwise).
+ */
+int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+            int32_t levels, void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
+
+/*
+ * norm_inf -- ||X||_inf = max_i sum_j |X_ij| of a dense row-major rows x cols
+ * device matrix; each row sum is accumulated left to right (as the oracle does), the max
+ * is order-free.  out_device: DEVICE pointer to one double, overwritten.
+ */
+int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, void* stream);
+
+/*
+ * mm_lambda -- the device-side lambda rule of mm_winograd_scaled applied to two host
+ * norms (for tests of the rule itself); returns lambda.  Runs on the host, no GPU needed.
+ */
+int32_t mm_lambda(double nA, double nB);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MM_B200_H */

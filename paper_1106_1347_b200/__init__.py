@@ -1,0 +1,241 @@
+"""B200-native FP64 matrix multiplication in the families of Hedtke, "Methods of Matrix
+Multiplication" (arXiv 1106.1347).
+
+Thin ctypes binding over the C ABI of ``libmm_b200.so`` (declared in ``include/mm.h``).
+This module only marshals arguments: every arithmetic step runs in the sm_100a kernels of
+the library.  PyTorch supplies device memory, streams and (in ``dist``) process groups.
+
+There is no CPU fallback: if the library is missing, or the device is not a B200
+(sm_100), every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import torch
+
+from . import build as _build
+
+__all__ = [
+    "MMError", "lib", "naive", "naive_on_array", "unroll2", "unroll3", "unroll4", "kahan", "winograd",
+    "winograd_scaled", "strassen", "strassen_winograd", "norm_inf", "matmul", "strassen_plan",
+    "workspace_size", "lambda_rule", "METHODS",
+]
+
+MM_NAIVE, MM_KAHAN, MM_WINOGRAD, MM_WINOGRAD_SCALED, MM_STRASSEN, MM_STRASSEN_WINOGRAD = range(6)
+METHODS = {
+    "naive": MM_NAIVE,
+    "kahan": MM_KAHAN,
+    "winograd": MM_WINOGRAD,
+    "winograd_scaled": MM_WINOGRAD_SCALED,
+    "strassen": MM_STRASSEN,
+    "strassen_winograd": MM_STRASSEN_WINOGRAD,
+}
+
+# every symbol include/mm.h declares
+EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winograd", "mm_winograd_scaled",
+           "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
+           "mm_lambda")
+
+
+class MMError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmm_b200.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB_PATH
+        if not os.path.exists(path):
+            raise MMError(f"{path} is missing: run __graft_entry__.build() (python -m paper_1106_1347_b200.build)")
+        L = ctypes.CDLL(path)
+        vp, i64, i32, sz, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p
+        L.mm_version.restype = ctypes.c_char_p
+        L.mm_status_string.restype = ctypes.c_char_p
+        L.mm_status_string.argtypes = [ctypes.c_int]
+        for n in ("mm_naive", "mm_kahan"):
+            getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp]
+        L.mm_winograd.argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
+        L.mm_winograd_scaled.argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, ctypes.POINTER(i32), vp]
+        for n in ("mm_strassen", "mm_strassen_winograd"):
+            getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, i32, vp, sz, vp]
+        L.mm_strassen_plan.argtypes = [i64, i64, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i64),
+                                       ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.mm_workspace_size.argtypes = [ctypes.c_int, i64, i64, i64, i32]
+        L.mm_workspace_size.restype = sz
+        L.mm_gemm.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64, i32, vp, sz, ctypes.POINTER(i32), vp]
+        L.norm_inf.argtypes = [dp, i64, i64, dp, vp]
+        L.mm_lambda.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.mm_lambda.restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise MMError(f"{what}: {lib().mm_status_string(rc).decode()} (status {rc})")
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream], device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _operands(A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor]):
+    if not (isinstance(A, torch.Tensor) and isinstance(B, torch.Tensor)):
+        raise TypeError("A and B must be torch tensors")
+    if A.dtype != torch.float64 or B.dtype != torch.float64:
+        raise ValueError("A and B must be float64 (the paper's entries are of type double)")
+    if A.dim() != 2 or B.dim() != 2:
+        raise ValueError("A and B must be matrices")
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"inner dimensions differ: {tuple(A.shape)} x {tuple(B.shape)}")
+    if not (A.is_cuda and B.is_cuda) or A.device != B.device:
+        raise ValueError("A and B must be CUDA tensors on one device (use matmul() for host tensors)")
+    if not (A.is_contiguous() and B.is_contiguous()):
+        raise ValueError("A and B must be contiguous row-major")
+    N, P = A.shape
+    M = B.shape[1]
+    if out is None:
+        out = torch.empty((N, M), dtype=torch.float64, device=A.device)
+    elif out.shape != (N, M) or out.dtype != torch.float64 or out.device != A.device or not out.is_contiguous():
+        raise ValueError("out must be a contiguous float64 N x M tensor on A's device")
+    return N, P, M, out
+
+
+# ---- workspace: grown on demand, then reused (no allocation on later calls) ----------
+_ws = {}
+
+
+def _workspace(nbytes: int, device) -> Tuple[int, int]:
+    if nbytes == 0:
+        return 0, 0
+    key = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _ws[key] = buf
+    return buf.data_ptr(), buf.numel()
+
+
+def release_workspace():
+    _ws.clear()
+
+
+def workspace_size(method: str, N: int, P: int, M: int, levels: int = 0) -> int:
+    return int(lib().mm_workspace_size(METHODS[method], N, P, M, levels))
+
+
+def strassen_plan(N: int, P: int, M: int, levels: int):
+    """(depth, Np, Pp, Mp) the library uses for this problem (levels=-1: the paper's plan)."""
+    d = ctypes.c_int32()
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().mm_strassen_plan(N, P, M, levels, ctypes.byref(d), ctypes.byref(a), ctypes.byref(b),
+                                  ctypes.byref(c)), "mm_strassen_plan")
+    return int(d.value), int(a.value), int(b.value), int(c.value)
+
+
+def lambda_rule(nA: float, nB: float) -> int:
+    return int(lib().mm_lambda(float(nA), float(nB)))
+
+
+def _gemm(method: int, name: str, A, B, out=None, levels: int = 0, stream=None, want_lambda=False):
+    N, P, M, out = _operands(A, B, out)
+    L = lib()
+    ws_bytes = int(L.mm_workspace_size(method, N, P, M, levels))
+    if method in (MM_STRASSEN, MM_STRASSEN_WINOGRAD) and ws_bytes == 0:
+        d = strassen_plan(N, P, M, levels)[0]
+        if d != 0:
+            raise MMError("bad Strassen plan")
+    ws_ptr, ws_len = _workspace(ws_bytes, A.device)
+    lam = ctypes.c_int32(0)
+    st = _stream_handle(stream, A.device)
+    rc = L.mm_gemm(method, A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, levels, ws_ptr, ws_len,
+                   ctypes.byref(lam) if want_lambda else None, st)
+    _check(rc, name)
+    if want_lambda:
+        return out, int(lam.value)
+    return out
+
+
+def naive(A, B, *, out=None, stream=None):
+    """NaivStandard on the FP64 tensor cores."""
+    return _gemm(MM_NAIVE, "mm_naive", A, B, out, stream=stream)
+
+
+# NaivOnArray and the unrolled variants compute the same product; on the GPU they are the
+# same DMMA kernel (their C loop shapes are prior art).
+naive_on_array = naive
+unroll2 = naive
+unroll3 = naive
+unroll4 = naive
+
+
+def kahan(A, B, *, out=None, stream=None):
+    """NaivKahan."""
+    return _gemm(MM_KAHAN, "mm_kahan", A, B, out, stream=stream)
+
+
+def winograd(A, B, *, out=None, stream=None):
+    """WinogradOriginal."""
+    return _gemm(MM_WINOGRAD, "mm_winograd", A, B, out, stream=stream)
+
+
+def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False):
+    """WinogradScaled.  return_lambda=True synchronises and returns (C, lambda)."""
+    return _gemm(MM_WINOGRAD_SCALED, "mm_winograd_scaled", A, B, out, stream=stream, want_lambda=return_lambda)
+
+
+def strassen(A, B, *, levels: int = 2, out=None, stream=None):
+    """StrassenNaiv; levels=-1 uses the paper's padding plan."""
+    return _gemm(MM_STRASSEN, "mm_strassen", A, B, out, levels=levels, stream=stream)
+
+
+def strassen_winograd(A, B, *, levels: int = 2, out=None, stream=None):
+    """StrassenWinograd."""
+    return _gemm(MM_STRASSEN_WINOGRAD, "mm_strassen_winograd", A, B, out, levels=levels, stream=stream)
+
+
+def norm_inf(X: torch.Tensor, *, out=None, stream=None) -> torch.Tensor:
+    """||X||_inf as a 1-element float64 device tensor."""
+    if X.dtype != torch.float64 or X.dim() != 2 or not X.is_cuda or not X.is_contiguous():
+        raise ValueError("X must be a contiguous float64 CUDA matrix")
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=X.device)
+    _check(lib().norm_inf(X.data_ptr(), X.shape[0], X.shape[1], out.data_ptr(), _stream_handle(stream, X.device)),
+           "norm_inf")
+    return out
+
+
+_FUNCS = {
+    "naive": naive, "kahan": kahan, "winograd": winograd, "winograd_scaled": winograd_scaled,
+    "strassen": strassen, "strassen_winograd": strassen_winograd,
+}
+
+
+def matmul(A: torch.Tensor, B: torch.Tensor, method: str = "naive", *, levels: int = 2, device=None,
+           stream=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The user-level call.  Device tensors run in place on their device; host tensors are
+    copied to `device` (default cuda:current), multiplied there and the product is copied back
+    into `out` (or a new host tensor) -- the end-to-end path bench.py's `e2e` times."""
+    f = _FUNCS[method]
+    kw = {"levels": levels} if method in ("strassen", "strassen_winograd") else {}
+    if A.is_cuda and B.is_cuda:
+        return f(A, B, out=out, stream=stream, **kw)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):
+        dA = A.to(dev, non_blocking=True)
+        dB = B.to(dev, non_blocking=True)
+        dC = f(dA, dB, stream=s, **kw)
+        if out is None:
+            out = torch.empty(dC.shape, dtype=dC.dtype, pin_memory=A.is_pinned())
+        out.copy_(dC, non_blocking=True)
+    s.synchronize()
+    return out

@@ -1,0 +1,226 @@
+// mm_abi.cu -- the extern "C" boundary declared in include/mm.h: argument validation,
+// workspace carving and kernel dispatch.  Every arithmetic step runs in the sm_100a kernels
+// included below; this file does no arithmetic on matrix data.
+#include "../../include/mm.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+#include "kahan.cuh"
+#include "norm_lambda.cuh"
+#include "strassen.cuh"
+#include "winograd.cuh"
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+int g_dev_ok[kMaxDevices];  // 0 unknown, 1 sm_100, -1 other
+int g_dev_sms[kMaxDevices];
+
+int check_device(int* sms_out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return MM_ERR_UNSUPPORTED;
+  }
+  if (dev < 0 || dev >= kMaxDevices) return MM_ERR_UNSUPPORTED;
+  if (g_dev_ok[dev] == 0) {
+    int major = 0, minor = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return MM_ERR_UNSUPPORTED;
+    }
+    g_dev_ok[dev] = (major == 10 && minor == 0) ? 1 : -1;
+    g_dev_sms[dev] = sms;
+  }
+  if (g_dev_ok[dev] != 1) return MM_ERR_UNSUPPORTED;
+  if (sms_out) *sms_out = g_dev_sms[dev];
+  return MM_OK;
+}
+
+bool mul_ok(int64_t a, int64_t b) { return a > 0 && b > 0 && a <= INT64_MAX / 8 / b; }
+
+bool overlaps(const void* p, int64_t pn, const void* q, int64_t qn) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p), a1 = a0 + uintptr_t(pn) * 8;
+  const uintptr_t b0 = reinterpret_cast<uintptr_t>(q), b1 = b0 + uintptr_t(qn) * 8;
+  return a0 < b1 && b0 < a1;
+}
+
+int check_abc(const double* A, const double* B, const double* C, int64_t N, int64_t P, int64_t M) {
+  if (!A || !B || !C) return MM_ERR_ARG;
+  if (N < 1 || P < 1 || M < 1) return MM_ERR_ARG;
+  if (!mul_ok(N, P) || !mul_ok(P, M) || !mul_ok(N, M)) return MM_ERR_ARG;
+  if (overlaps(C, N * M, A, N * P) || overlaps(C, N * M, B, P * M)) return MM_ERR_ALIAS;
+  return MM_OK;
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return MM_OK;
+  cudaGetLastError();
+  return MM_ERR_CUDA;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t winograd_ws(int64_t N, int64_t M) {
+  return mmk::align256(size_t(N) * 8) + mmk::align256(size_t(M) * 8);
+}
+constexpr size_t kScaledHeader = 256;  // norms[2] (u64), scale[2] (double), lambda (int)
+
+}  // namespace
+
+extern "C" {
+
+const char* mm_version(void) { return "paper_1106_1347_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+const char* mm_status_string(int status) {
+  switch (status) {
+    case MM_OK: return "ok";
+    case MM_ERR_ARG: return "invalid argument (NULL pointer, size < 1 or overflow, bad levels)";
+    case MM_ERR_ALIAS: return "C overlaps A or B";
+    case MM_ERR_WORKSPACE: return "workspace too small (see mm_workspace_size)";
+    case MM_ERR_CUDA: return "CUDA launch or runtime error";
+    case MM_ERR_UNSUPPORTED: return "current device is not sm_100 (B200); no fallback exists";
+    default: return "unknown status";
+  }
+}
+
+int32_t mm_lambda(double nA, double nB) { return mmk::lambda_rule(nA, nB); }
+
+int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  if ((rc = check_device(nullptr))) return rc;
+  mmk::GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
+  return cuda_status(mmk::launch_dgemm(pr, S(stream)));
+}
+
+int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  if ((rc = check_device(nullptr))) return rc;
+  return cuda_status(mmk::launch_kahan(A, B, C, N, P, M, S(stream)));
+}
+
+size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels) {
+  if (N < 1 || P < 1 || M < 1) return 0;
+  switch (method) {
+    case MM_NAIVE:
+    case MM_KAHAN: return 0;
+    case MM_WINOGRAD: return winograd_ws(N, M);
+    case MM_WINOGRAD_SCALED: return kScaledHeader + winograd_ws(N, M);
+    case MM_STRASSEN:
+    case MM_STRASSEN_WINOGRAD: {
+      mmk::StrassenPlan pl;
+      if (!mmk::make_strassen_plan(N, P, M, levels, &pl)) return 0;
+      return pl.total;
+    }
+    default: return 0;
+  }
+}
+
+int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* workspace,
+                size_t ws_bytes, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  if (!workspace) return MM_ERR_ARG;
+  if (ws_bytes < winograd_ws(N, M)) return MM_ERR_WORKSPACE;
+  if ((rc = check_device(nullptr))) return rc;
+  double* y = static_cast<double*>(workspace);
+  double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N) * 8));
+  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, mmk::WinogradScale{nullptr}, S(stream)));
+}
+
+int mm_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                       void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  if (!workspace) return MM_ERR_ARG;
+  if (ws_bytes < kScaledHeader + winograd_ws(N, M)) return MM_ERR_WORKSPACE;
+  if ((rc = check_device(nullptr))) return rc;
+  char* ws = static_cast<char*>(workspace);
+  auto* norms = reinterpret_cast<unsigned long long*>(ws);
+  auto* scale = reinterpret_cast<double*>(ws + 16);
+  auto* lam = reinterpret_cast<int*>(ws + 32);
+  double* y = reinterpret_cast<double*>(ws + kScaledHeader);
+  double* z = reinterpret_cast<double*>(ws + kScaledHeader + mmk::align256(size_t(N) * 8));
+  cudaStream_t st = S(stream);
+  cudaError_t e = mmk::launch_norm_inf(A, N, P, norms, st);
+  if (e == cudaSuccess) e = mmk::launch_norm_inf(B, P, M, norms + 1, st);
+  if (e == cudaSuccess) {
+    mmk::lambda_kernel<<<1, 32, 0, st>>>(norms, lam, scale);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = mmk::launch_winograd(A, B, C, y, z, N, P, M, mmk::WinogradScale{scale}, st);
+  if (e == cudaSuccess && lambda_out) {
+    e = cudaMemcpyAsync(lambda_out, lam, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  return cuda_status(e);
+}
+
+int mm_strassen_plan(int64_t N, int64_t P, int64_t M, int32_t levels, int32_t* depth_out, int64_t* Np_out,
+                     int64_t* Pp_out, int64_t* Mp_out) {
+  mmk::StrassenPlan pl;
+  if (!mmk::make_strassen_plan(N, P, M, levels, &pl)) return MM_ERR_ARG;
+  if (depth_out) *depth_out = pl.depth;
+  if (Np_out) *Np_out = pl.Np;
+  if (Pp_out) *Pp_out = pl.Pp;
+  if (Mp_out) *Mp_out = pl.Mp;
+  return MM_OK;
+}
+
+static int strassen_common(int variant, const double* A, const double* B, double* C, int64_t N, int64_t P,
+                           int64_t M, int32_t levels, void* workspace, size_t ws_bytes, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  mmk::StrassenPlan pl;
+  if (!mmk::make_strassen_plan(N, P, M, levels, &pl)) return MM_ERR_ARG;
+  if (pl.total > 0 && (!workspace || ws_bytes < pl.total)) return MM_ERR_WORKSPACE;
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
+  char* ws = static_cast<char*>(workspace);
+  cudaError_t e = variant == mmk::SV_NAIV ? mmk::run_strassen<mmk::SV_NAIV>(A, B, C, N, P, M, pl, ws, sms, S(stream))
+                                          : mmk::run_strassen<mmk::SV_WINOGRAD>(A, B, C, N, P, M, pl, ws, sms,
+                                                                               S(stream));
+  return cuda_status(e);
+}
+
+int mm_strassen(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, int32_t levels,
+                void* workspace, size_t ws_bytes, void* stream) {
+  return strassen_common(mmk::SV_NAIV, A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+}
+
+int mm_strassen_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                         int32_t levels, void* workspace, size_t ws_bytes, void* stream) {
+  return strassen_common(mmk::SV_WINOGRAD, A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+}
+
+int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+            int32_t levels, void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream) {
+  switch (method) {
+    case MM_NAIVE: return mm_naive(A, B, C, N, P, M, stream);
+    case MM_KAHAN: return mm_kahan(A, B, C, N, P, M, stream);
+    case MM_WINOGRAD: return mm_winograd(A, B, C, N, P, M, workspace, ws_bytes, stream);
+    case MM_WINOGRAD_SCALED: return mm_winograd_scaled(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
+    case MM_STRASSEN: return mm_strassen(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+    case MM_STRASSEN_WINOGRAD: return mm_strassen_winograd(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+    default: return MM_ERR_ARG;
+  }
+}
+
+int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, void* stream) {
+  if (!X || !out_device || rows < 1 || cols < 1 || !mul_ok(rows, cols)) return MM_ERR_ARG;
+  int rc = check_device(nullptr);
+  if (rc) return rc;
+  return cuda_status(
+      mmk::launch_norm_inf(X, rows, cols, reinterpret_cast<unsigned long long*>(out_device), S(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,368 @@
+// strassen.cuh -- K6/K7/K8: StrassenNaiv and StrassenWinograd as a
+// breadth-first recursion over a workspace arena.
+//
+//  level l holds 7^l nodes; node q's operands are dense [n_l x p_l] / [p_l x m_l] blocks at
+//  q * n_l * p_l of the level buffer; child t (t = 0..6 for H_{t+1}) of node q is node 7q + t.
+//
+//  * form kernel (one launch per level and side): reads the four quadrants X11, X12, X21,
+//    X22 of every node once and writes the seven child operands, fusing the paper's block
+//    additions (P:271-277 / P:300-306) in registers with exactly the oracle's per-element
+//    operations and order (e.g. A2 = A22 - (A11 - A21)).  At level 0 it reads the caller's A
+//    or B with the zero embedding of P:286 applied on the fly (no padded copy).
+//  * the 7^d leaf products H = S T run as ONE batched DMMA GEMM launch (gemm_dmma.cuh).
+//  * combine kernel (one launch per level): reads H_1..H_7 of every node once and writes
+//    the four C quadrants (P:279-282 / P:307-311, left to right as displayed); at level 0
+//    it writes straight into the caller's C, dropping the padding (the "extract" of P:286).
+// All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
+#pragma once
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+
+namespace mmk {
+
+constexpr int SV_NAIV = 0, SV_WINOGRAD = 1;
+
+struct FormArgs {
+  const double* src;      // parent level: cnt nodes
+  int64_t src_pitch;      // row pitch of a parent node (elements)
+  int64_t src_stride;     // distance between parent nodes (elements)
+  int64_t rows_valid;     // rows of the parent that hold data (the rest are the zero embedding)
+  int64_t cols_valid;
+  double* dst;            // child level: 7 cnt dense nodes of h_rows x h_cols
+  int64_t h_rows, h_cols; // child (= quadrant) dims
+  int64_t cnt;
+};
+
+template <int VEC>
+__device__ __forceinline__ void ld_quad(const FormArgs& a, const double* base, int64_t r, int64_t c, double* v) {
+  // v[0..VEC) = parent[r][c .. c+VEC) with the zero embedding outside rows_valid x cols_valid
+  const double* p = base + r * a.src_pitch + c;
+  if (VEC == 2 && r < a.rows_valid && c + 1 < a.cols_valid) {
+    double2 w = *reinterpret_cast<const double2*>(p);
+    v[0] = w.x;
+    v[1] = w.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) v[e] = (r < a.rows_valid && c + e < a.cols_valid) ? p[e] : 0.0;
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_vec(double* p, const double* v) {
+  if (VEC == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  } else {
+    p[0] = v[0];
+  }
+}
+
+// SIDE 0 = left operands (from A), SIDE 1 = right operands (from B)
+template <int VARIANT, int SIDE, int VEC>
+__global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a) {
+  const int64_t hv = a.h_cols / VEC;
+  const int64_t per_node = a.h_rows * hv;
+  const int64_t total = a.cnt * per_node;
+  const int64_t child_elems = a.h_rows * a.h_cols;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = idx / per_node;
+    const int64_t rem = idx - q * per_node;
+    const int64_t i = rem / hv;
+    const int64_t j = (rem - i * hv) * VEC;
+    const double* base = a.src + q * a.src_stride;
+    double x11[VEC], x12[VEC], x21[VEC], x22[VEC];
+    ld_quad<VEC>(a, base, i, j, x11);
+    ld_quad<VEC>(a, base, i, j + a.h_cols, x12);
+    ld_quad<VEC>(a, base, i + a.h_rows, j, x21);
+    ld_quad<VEC>(a, base, i + a.h_rows, j + a.h_cols, x22);
+    double o[7][VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      if (VARIANT == SV_NAIV) {
+        if (SIDE == 0) {              // P:271-277, left factors
+          o[0][e] = dadd(x11[e], x22[e]);  // H1: A11 + A22
+          o[1][e] = dadd(x21[e], x22[e]);  // H2: A21 + A22
+          o[2][e] = x11[e];                // H3: A11
+          o[3][e] = x22[e];                // H4: A22
+          o[4][e] = dadd(x11[e], x12[e]);  // H5: A11 + A12
+          o[5][e] = dsub(x21[e], x11[e]);  // H6: A21 - A11
+          o[6][e] = dsub(x12[e], x22[e]);  // H7: A12 - A22
+        } else {                      // right factors
+          o[0][e] = dadd(x11[e], x22[e]);  // H1: B11 + B22
+          o[1][e] = x11[e];                // H2: B11
+          o[2][e] = dsub(x12[e], x22[e]);  // H3: B12 - B22
+          o[3][e] = dsub(x21[e], x11[e]);  // H4: B21 - B11
+          o[4][e] = x22[e];                // H5: B22
+          o[5][e] = dadd(x11[e], x12[e]);  // H6: B11 + B12
+          o[6][e] = dadd(x21[e], x22[e]);  // H7: B21 + B22
+        }
+      } else {
+        if (SIDE == 0) {
+          const double a1 = dsub(x11[e], x21[e]);  // A1 = A11 - A21
+          const double a2 = dsub(x22[e], a1);      // A2 = A22 - A1
+          o[0][e] = x11[e];                        // H1: A11
+          o[1][e] = x12[e];                        // H2: A12
+          o[2][e] = a2;                            // H3: A2
+          o[3][e] = dadd(x21[e], x22[e]);          // H4: A21 + A22
+          o[4][e] = a1;                            // H5: A1
+          o[5][e] = dsub(x12[e], a2);              // H6: A12 - A2
+          o[6][e] = x22[e];                        // H7: A22
+        } else {
+          const double b1 = dsub(x22[e], x12[e]);  // B1 = B22 - B12
+          const double b2 = dadd(b1, x11[e]);      // B2 = B1 + B11
+          o[0][e] = x11[e];                        // H1: B11
+          o[1][e] = x21[e];                        // H2: B21
+          o[2][e] = b2;                            // H3: B2
+          o[3][e] = dsub(x12[e], x11[e]);          // H4: B12 - B11
+          o[4][e] = b1;                            // H5: B1
+          o[5][e] = x22[e];                        // H6: B22
+          o[6][e] = dsub(x21[e], b2);              // H7: B21 - B2
+        }
+      }
+    }
+    double* d0 = a.dst + (7 * q) * child_elems + i * a.h_cols + j;
+#pragma unroll
+    for (int t = 0; t < 7; ++t) st_vec<VEC>(d0 + t * child_elems, o[t]);
+  }
+}
+
+struct CombineArgs {
+  const double* H;         // 7 cnt dense nodes of h_rows x h_cols
+  double* dst;             // cnt parent nodes
+  int64_t dst_pitch, dst_stride;
+  int64_t rows_valid, cols_valid;  // parent region that is stored (extraction at level 0)
+  int64_t h_rows, h_cols, cnt;
+};
+
+template <int VEC>
+__device__ __forceinline__ void st_quad(const CombineArgs& a, double* base, int64_t r, int64_t c, const double* v) {
+  double* p = base + r * a.dst_pitch + c;
+  if (VEC == 2 && r < a.rows_valid && c + 1 < a.cols_valid) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (r < a.rows_valid && c + e < a.cols_valid) p[e] = v[e];
+  }
+}
+
+template <int VARIANT, int VEC>
+__global__ void __launch_bounds__(256) strassen_combine_kernel(CombineArgs a) {
+  const int64_t hv = a.h_cols / VEC;
+  const int64_t per_node = a.h_rows * hv;
+  const int64_t total = a.cnt * per_node;
+  const int64_t child_elems = a.h_rows * a.h_cols;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = idx / per_node;
+    const int64_t rem = idx - q * per_node;
+    const int64_t i = rem / hv;
+    const int64_t j = (rem - i * hv) * VEC;
+    const double* h0 = a.H + (7 * q) * child_elems + i * a.h_cols + j;
+    double h[7][VEC];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+      if (VEC == 2) {
+        double2 w = *reinterpret_cast<const double2*>(h0 + t * child_elems);
+        h[t][0] = w.x;
+        h[t][1] = w.y;
+      } else {
+        h[t][0] = h0[t * child_elems];
+      }
+    }
+    double c11[VEC], c12[VEC], c21[VEC], c22[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const double H1 = h[0][e], H2 = h[1][e], H3 = h[2][e], H4 = h[3][e], H5 = h[4][e], H6 = h[5][e],
+                   H7 = h[6][e];
+      if (VARIANT == SV_NAIV) {  // P:279-282, left to right
+        c11[e] = dadd(dsub(dadd(H1, H4), H5), H7);
+        c12[e] = dadd(H3, H5);
+        c21[e] = dadd(H2, H4);
+        c22[e] = dadd(dsub(dadd(H1, H3), H2), H6);
+      } else {
+        const double H8 = dadd(H1, H3);
+        const double H9 = dadd(H8, H4);
+        c11[e] = dadd(H1, H2);
+        c12[e] = dadd(H9, H6);
+        c21[e] = dadd(dadd(H8, H5), H7);
+        c22[e] = dadd(H9, H5);
+      }
+    }
+    double* base = a.dst + q * a.dst_stride;
+    st_quad<VEC>(a, base, i, j, c11);
+    st_quad<VEC>(a, base, i, j + a.h_cols, c12);
+    st_quad<VEC>(a, base, i + a.h_rows, j, c21);
+    st_quad<VEC>(a, base, i + a.h_rows, j + a.h_cols, c22);
+  }
+}
+
+// ---------------------------------------------------------------- plan + arena
+struct StrassenPlan {
+  int depth;
+  int64_t Np, Pp, Mp;
+  // arena offsets (bytes)
+  size_t offS[2], offT[2], offH, offC[2], total;
+};
+
+inline int64_t ipow7(int d) {
+  int64_t r = 1;
+  for (int i = 0; i < d; ++i) r *= 7;
+  return r;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// levels >= 0: pad each dim to a multiple of 2^(levels+1) (keeps every level's row pitch
+// even, so 16-byte vectors apply); levels == -1: the paper's square plan.
+inline bool make_strassen_plan(int64_t N, int64_t P, int64_t M, int levels, StrassenPlan* pl) {
+  if (N < 1 || P < 1 || M < 1 || levels < -1 || levels > 8) return false;
+  if (levels == -1) {
+    int64_t X = N > P ? N : P;
+    X = X > M ? X : M;
+    int lg = 0;
+    while ((int64_t(1) << (lg + 1)) <= X) ++lg;
+    int k = lg - 4;
+    if (k < 0) k = 0;
+    const int64_t m = (X >> k) + 1;
+    const int64_t Y = m << k;
+    pl->depth = k;
+    pl->Np = pl->Pp = pl->Mp = Y;
+    if (k > 8) return false;
+  } else {
+    const int64_t q = int64_t(2) << levels;
+    pl->depth = levels;
+    pl->Np = cdiv(N, q) * q;
+    pl->Pp = cdiv(P, q) * q;
+    pl->Mp = cdiv(M, q) * q;
+  }
+  const int d = pl->depth;
+  auto lvl = [&](int l, int64_t r, int64_t c) -> size_t {  // bytes of level l for an r x c root
+    if (l <= 0) return 0;
+    return size_t(ipow7(l)) * size_t(r >> l) * size_t(c >> l) * sizeof(double);
+  };
+  size_t off = 0;
+  const size_t s0 = lvl(d, pl->Np, pl->Pp), s1 = lvl(d - 1, pl->Np, pl->Pp);
+  const size_t t0 = lvl(d, pl->Pp, pl->Mp), t1 = lvl(d - 1, pl->Pp, pl->Mp);
+  const size_t h = lvl(d, pl->Np, pl->Mp);
+  const size_t c0 = lvl(d - 1, pl->Np, pl->Mp), c1 = lvl(d - 2, pl->Np, pl->Mp);
+  pl->offS[0] = off; off = align256(off + s0);
+  pl->offS[1] = off; off = align256(off + s1);
+  pl->offT[0] = off; off = align256(off + t0);
+  pl->offT[1] = off; off = align256(off + t1);
+  pl->offH = off;    off = align256(off + h);
+  pl->offC[0] = off; off = align256(off + c0);
+  pl->offC[1] = off; off = align256(off + c1);
+  pl->total = (d == 0) ? 0 : off;
+  return true;
+}
+
+inline unsigned grid_for(int64_t work, int sms) {
+  int64_t b = cdiv(work, 256);
+  int64_t cap = int64_t(sms) * 16;  // grid-stride beyond 16 blocks per SM
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return unsigned(b);
+}
+
+template <int VARIANT>
+cudaError_t launch_form_level(int side, const FormArgs& fa, bool vec, int sms, cudaStream_t st) {
+  const int64_t work = fa.cnt * fa.h_rows * (vec ? fa.h_cols / 2 : fa.h_cols);
+  const unsigned g = grid_for(work, sms);
+  if (side == 0) {
+    if (vec) strassen_form_kernel<VARIANT, 0, 2><<<g, 256, 0, st>>>(fa);
+    else strassen_form_kernel<VARIANT, 0, 1><<<g, 256, 0, st>>>(fa);
+  } else {
+    if (vec) strassen_form_kernel<VARIANT, 1, 2><<<g, 256, 0, st>>>(fa);
+    else strassen_form_kernel<VARIANT, 1, 1><<<g, 256, 0, st>>>(fa);
+  }
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
+cudaError_t launch_combine_level(const CombineArgs& ca, bool vec, int sms, cudaStream_t st) {
+  const int64_t work = ca.cnt * ca.h_rows * (vec ? ca.h_cols / 2 : ca.h_cols);
+  const unsigned g = grid_for(work, sms);
+  if (vec) strassen_combine_kernel<VARIANT, 2><<<g, 256, 0, st>>>(ca);
+  else strassen_combine_kernel<VARIANT, 1><<<g, 256, 0, st>>>(ca);
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
+cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                         const StrassenPlan& pl, char* ws, int sms, cudaStream_t st) {
+  const int d = pl.depth;
+  if (d == 0) {
+    GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
+    return launch_dgemm(pr, st);
+  }
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  cudaError_t e;
+  double* S[2] = {reinterpret_cast<double*>(ws + pl.offS[0]), reinterpret_cast<double*>(ws + pl.offS[1])};
+  double* T[2] = {reinterpret_cast<double*>(ws + pl.offT[0]), reinterpret_cast<double*>(ws + pl.offT[1])};
+  double* Hb = reinterpret_cast<double*>(ws + pl.offH);
+  double* Cb[2] = {reinterpret_cast<double*>(ws + pl.offC[0]), reinterpret_cast<double*>(ws + pl.offC[1])};
+  // level l >= 1 of S/T lives in buffer (d - l) % 2 ; combination level l >= 1 in Cb[(d - 1 - l) % 2]
+  for (int side = 0; side < 2; ++side) {
+    const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
+    double** buf = side == 0 ? S : T;
+    for (int l = 0; l < d; ++l) {
+      FormArgs fa;
+      const int64_t r_l = R >> l, c_l = Ccols >> l;
+      if (l == 0) {
+        fa.src = side == 0 ? A : B;
+        fa.src_pitch = side == 0 ? P : M;
+        fa.src_stride = 0;
+        fa.rows_valid = side == 0 ? N : P;
+        fa.cols_valid = side == 0 ? P : M;
+      } else {
+        fa.src = buf[(d - l) % 2];
+        fa.src_pitch = c_l;
+        fa.src_stride = r_l * c_l;
+        fa.rows_valid = r_l;
+        fa.cols_valid = c_l;
+      }
+      fa.dst = buf[(d - l - 1) % 2];
+      fa.h_rows = r_l / 2;
+      fa.h_cols = c_l / 2;
+      fa.cnt = ipow7(l);
+      const bool vec = (fa.h_cols % 2 == 0) && (fa.src_pitch % 2 == 0) && al16(fa.src);
+      e = launch_form_level<VARIANT>(side, fa, vec, sms, st);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  // the 7^d leaf products, one batched DMMA launch
+  {
+    const int64_t n = pl.Np >> d, p = pl.Pp >> d, m = pl.Mp >> d;
+    GemmProblem pr{S[0], T[0], Hb, n, p, m, p, m, m, n * p, p * m, n * m, ipow7(d)};
+    e = launch_dgemm(pr, st);
+    if (e != cudaSuccess) return e;
+  }
+  for (int l = d - 1; l >= 0; --l) {
+    CombineArgs ca;
+    const int64_t r_l = pl.Np >> l, c_l = pl.Mp >> l;
+    ca.H = (l == d - 1) ? Hb : Cb[(d - 1 - (l + 1)) % 2];
+    if (l == 0) {
+      ca.dst = C;
+      ca.dst_pitch = M;
+      ca.dst_stride = 0;
+      ca.rows_valid = N;
+      ca.cols_valid = M;
+    } else {
+      ca.dst = Cb[(d - 1 - l) % 2];
+      ca.dst_pitch = c_l;
+      ca.dst_stride = r_l * c_l;
+      ca.rows_valid = r_l;
+      ca.cols_valid = c_l;
+    }
+    ca.h_rows = r_l / 2;
+    ca.h_cols = c_l / 2;
+    ca.cnt = ipow7(l);
+    const bool vec = (ca.h_cols % 2 == 0) && (ca.dst_pitch % 2 == 0) && al16(ca.dst);
+    e = launch_combine_level<VARIANT>(ca, vec, sms, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace mmk

@@ -1,0 +1,300 @@
+// winograd.cuh -- K3: WinogradOriginal / WinogradScaled.
+//
+// 0-based form of P:189-192 (reading R5): gamma = floor(P/2),
+//   y_i = sum_{j<gamma} A[i][2j] A[i][2j+1]            z_k = sum_{j<gamma} B[2j][k] B[2j+1][k]
+//   acc_ik = sum_{j<gamma} (A[i][2j] + B[2j+1][k]) (A[i][2j+1] + B[2j][k])
+//   C_ik = (acc_ik - y_i) - z_k  [ + A[i][P-1] B[P-1][k] when P is odd ]
+// Sums run in increasing j, every op is a separately rounded FP64 SIMT op, so the result
+// equals the oracle's or_winograd_original bit for bit -- required, because on ill-scaled
+// inputs (config c3) two equally valid summation orders differ by ~50 in the inf-norm.
+//
+// SCALED: the operands are 2^lambda A and 2^-lambda B (exact power-of-two
+// scalings, the oracle's or_scalar_mul), lambda read from device memory written by
+// lambda_kernel, so no host round trip.  Scaling is applied once per staged element in
+// shared memory and in the y/z prologue, never per use.
+//
+// Kernels:
+//  * winograd_yz_kernel: y (one thread per row, A staged through shared memory in
+//    coalesced 32 x 32 tiles) and z (one thread per column, coalesced) -- sequential sums.
+//  * winograd_kernel: CTA 64 x 128, 256 threads, 4 x 8 outputs per thread; the pair loop
+//    covers columns 0..2*gamma-1 only (the odd column never enters acc).
+#pragma once
+#include "common.cuh"
+
+namespace mmk {
+
+struct WinogradScale {
+  const double* sAB;  // device: [0] = 2^lambda, [1] = 2^-lambda ; nullptr = unscaled
+};
+
+// ---------------------------------------------------------------- y / z prologue
+namespace wyz {
+constexpr int THREADS = 128;  // rows (or columns) per block
+constexpr int TILE_K = 32;    // columns of A staged per step (16 pairs)
+}  // namespace wyz
+
+// blocks [0, nb_y) compute y for rows [128 b, 128 b + 128); blocks [nb_y, ...) compute z.
+__global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double* __restrict__ A,
+                                                                   const double* __restrict__ B,
+                                                                   double* __restrict__ y, double* __restrict__ z,
+                                                                   int64_t N, int64_t P, int64_t M, int nb_y,
+                                                                   WinogradScale sc) {
+  using namespace wyz;
+  __shared__ double tileA[THREADS][TILE_K + 1];
+  const int tid = threadIdx.x;
+  const int64_t gamma = P / 2;
+  const double sa = sc.sAB ? sc.sAB[0] : 1.0;
+  const double sb = sc.sAB ? sc.sAB[1] : 1.0;
+  if (int(blockIdx.x) < nb_y) {
+    const int64_t r0 = int64_t(blockIdx.x) * THREADS;
+    const int64_t kend = 2 * gamma;
+    double acc = 0.0;
+    for (int64_t k0 = 0; k0 < kend; k0 += TILE_K) {
+      // coalesced stage of rows r0..r0+127, columns k0..k0+31: each warp reads 32 consecutive doubles of a row
+      __syncthreads();
+      for (int e = tid; e < THREADS * TILE_K; e += THREADS) {
+        const int rr = e / TILE_K, kk = e % TILE_K;
+        const int64_t gr = r0 + rr, gk = k0 + kk;
+        double v = (gr < N && gk < kend) ? A[gr * P + gk] : 0.0;
+        if (sc.sAB) v = dmul(sa, v);
+        tileA[rr][kk] = v;
+      }
+      __syncthreads();
+      const int64_t rem_k = kend - k0;
+      const int npairs = int(rem_k < TILE_K ? rem_k : TILE_K) / 2;
+      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tileA[tid][2 * j], tileA[tid][2 * j + 1]));
+    }
+    const int64_t row = r0 + tid;
+    if (row < N) y[row] = acc;
+  } else {
+    const int64_t col = int64_t(blockIdx.x - nb_y) * THREADS + tid;
+    if (col >= M) return;
+    double acc = 0.0;
+    for (int64_t j = 0; j < gamma; ++j) {
+      double b0 = B[(2 * j) * M + col], b1 = B[(2 * j + 1) * M + col];
+      if (sc.sAB) {
+        b0 = dmul(sb, b0);
+        b1 = dmul(sb, b1);
+      }
+      acc = dadd(acc, dmul(b0, b1));
+    }
+    z[col] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- main pair-sum kernel
+namespace wino {
+constexpr int BM = 64, BN = 128, BK = 16, THREADS = 256, STAGES = 3;
+constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
+constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
+}  // namespace wino
+
+// Kend = 2*gamma: columns/rows >= Kend are zero-filled (the odd column is excluded).
+template <int AV, int BV>
+__device__ __forceinline__ void wino_load_tile(double* As, double* Bs, const double* __restrict__ A,
+                                               const double* __restrict__ B, int64_t N, int64_t P, int64_t M,
+                                               int64_t Kend, int64_t m0, int64_t n0, int64_t k0, int tid) {
+  using namespace wino;
+  if (AV == 2) {
+#pragma unroll
+    for (int i = 0; i < (A_ELEMS / 2) / THREADS; ++i) {
+      int c = tid + i * THREADS;
+      int r = c >> 3, kp = (c & 7) * 2;
+      int64_t gm = m0 + r, gk = k0 + kp;
+      bool v = gm < N && gk < Kend;
+      cp_async16(As + r * BK + kp, v ? A + gm * P + gk : A, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < A_ELEMS / THREADS; ++i) {
+      int e = tid + i * THREADS;
+      int r = e >> 4, kk = e & 15;
+      int64_t gm = m0 + r, gk = k0 + kk;
+      bool v = gm < N && gk < Kend;
+      cp_async8(As + r * BK + kk, v ? A + gm * P + gk : A, v);
+    }
+  }
+  if (BV == 2) {
+#pragma unroll
+    for (int i = 0; i < (B_ELEMS / 2) / THREADS; ++i) {
+      int c = tid + i * THREADS;
+      int kr = c >> 6, np = (c & 63) * 2;
+      int64_t gk = k0 + kr, gn = n0 + np;
+      bool v = gk < Kend && gn < M;
+      cp_async16(Bs + kr * BN + np, v ? B + gk * M + gn : B, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < B_ELEMS / THREADS; ++i) {
+      int e = tid + i * THREADS;
+      int kr = e >> 7, nn = e & 127;
+      int64_t gk = k0 + kr, gn = n0 + nn;
+      bool v = gk < Kend && gn < M;
+      cp_async8(Bs + kr * BN + nn, v ? B + gk * M + gn : B, v);
+    }
+  }
+}
+
+// scale, in place, exactly the shared elements this thread copied (after its cp.async completed)
+__device__ __forceinline__ void wino_scale_tile(double* As, double* Bs, double sa, double sb, int tid) {
+  using namespace wino;
+  for (int e = tid; e < A_ELEMS; e += THREADS) As[e] = dmul(sa, As[e]);
+  for (int e = tid; e < B_ELEMS; e += THREADS) Bs[e] = dmul(sb, Bs[e]);
+}
+
+template <int AV, int BV, int CV, bool SCALED>
+__global__ void __launch_bounds__(wino::THREADS, 1)
+    winograd_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                    const double* __restrict__ y, const double* __restrict__ z, int64_t N, int64_t P, int64_t M,
+                    WinogradScale sc) {
+  using namespace wino;
+  extern __shared__ __align__(128) double smem[];
+  double* As_base = smem;
+  double* Bs_base = smem + STAGES * A_ELEMS;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int64_t Kend = 2 * (P / 2);
+  double sa = 1.0, sb = 1.0;
+  if (SCALED) {
+    sa = sc.sAB[0];
+    sb = sc.sAB[1];
+  }
+
+  double acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  const int KT = int(cdiv(Kend, BK));
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < KT)
+      wino_load_tile<AV, BV>(As_base + st * A_ELEMS, Bs_base + st * B_ELEMS, A, B, N, P, M, Kend, m0, n0,
+                             int64_t(st) * BK, tid);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    if (SCALED) {
+      // each element was copied by thread (element index % THREADS) in the 8-byte loaders and
+      // by a fixed thread per 16-byte chunk otherwise; a barrier before scaling makes any
+      // element visible to whichever thread scales it.
+      __syncthreads();
+      wino_scale_tile(As_base + (kt % STAGES) * A_ELEMS, Bs_base + (kt % STAGES) * B_ELEMS, sa, sb, tid);
+    }
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT)
+        wino_load_tile<AV, BV>(As_base + (nk % STAGES) * A_ELEMS, Bs_base + (nk % STAGES) * B_ELEMS, A, B, N, P, M,
+                               Kend, m0, n0, int64_t(nk) * BK, tid);
+      cp_async_commit();
+    }
+    const double* As = As_base + (kt % STAGES) * A_ELEMS;
+    const double* Bs = Bs_base + (kt % STAGES) * B_ELEMS;
+    // zero-filled pairs past Kend add (0+0)(0+0) = +0 to acc, which leaves acc unchanged
+    // (acc starts at +0 and can never become -0), so the last tile needs no guard.
+#pragma unroll 2
+    for (int jp = 0; jp < BK / 2; ++jp) {
+      double a0[4], a1[4], b0[8], b1[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2 v = *reinterpret_cast<const double2*>(As + (4 * ty + i) * BK + 2 * jp);
+        a0[i] = v.x;
+        a1[i] = v.y;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double2 u = *reinterpret_cast<const double2*>(Bs + (2 * jp) * BN + 2 * tx + 32 * c);
+        double2 w = *reinterpret_cast<const double2*>(Bs + (2 * jp + 1) * BN + 2 * tx + 32 * c);
+        b0[2 * c] = u.x;
+        b0[2 * c + 1] = u.y;
+        b1[2 * c] = w.x;
+        b1[2 * c + 1] = w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool odd = (P & 1) != 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + 4 * ty + i;
+    if (row >= N) continue;
+    const double yi = y[row];
+    double alast = 0.0;
+    if (odd) {
+      alast = A[row * P + (P - 1)];
+      if (SCALED) alast = dmul(sa, alast);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t col = n0 + 2 * tx + 32 * c;
+      double out[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t cc = col + e;
+        double v = 0.0;
+        if (cc < M) {
+          v = dsub(dsub(acc[i][2 * c + e], yi), z[cc]);
+          if (odd) {
+            double blast = B[(P - 1) * M + cc];
+            if (SCALED) blast = dmul(sb, blast);
+            v = dadd(v, dmul(alast, blast));
+          }
+        }
+        out[e] = v;
+      }
+      if (CV == 2 && col + 1 < M) {
+        *reinterpret_cast<double2*>(C + row * M + col) = make_double2(out[0], out[1]);
+      } else {
+        if (col < M) C[row * M + col] = out[0];
+        if (col + 1 < M) C[row * M + col + 1] = out[1];
+      }
+    }
+  }
+}
+
+template <int AV, int BV, int CV, bool SCALED>
+cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const double* y, const double* z,
+                              int64_t N, int64_t P, int64_t M, WinogradScale sc, cudaStream_t st) {
+  using namespace wino;
+  auto kern = winograd_kernel<AV, BV, CV, SCALED>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(unsigned(cdiv(M, BN)), unsigned(cdiv(N, BM)));
+  kern<<<grid, THREADS, SMEM, st>>>(A, B, C, y, z, N, P, M, sc);
+  return cudaGetLastError();
+}
+
+// y, z: device buffers of N and M doubles.  sc.sAB == nullptr -> WinogradOriginal.
+inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
+                                   int64_t P, int64_t M, WinogradScale sc, cudaStream_t st) {
+  const int nb_y = int(cdiv(N, wyz::THREADS));
+  const int nb_z = int(cdiv(M, wyz::THREADS));
+  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y, sc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
+  const bool s = sc.sAB != nullptr;
+  if (av && bv && cv)
+    return s ? launch_winograd_t<2, 2, 2, true>(A, B, C, y, z, N, P, M, sc, st)
+             : launch_winograd_t<2, 2, 2, false>(A, B, C, y, z, N, P, M, sc, st);
+  if (bv && cv)
+    return s ? launch_winograd_t<1, 2, 2, true>(A, B, C, y, z, N, P, M, sc, st)
+             : launch_winograd_t<1, 2, 2, false>(A, B, C, y, z, N, P, M, sc, st);
+  return s ? launch_winograd_t<1, 1, 1, true>(A, B, C, y, z, N, P, M, sc, st)
+           : launch_winograd_t<1, 1, 1, false>(A, B, C, y, z, N, P, M, sc, st);
+}
+
+}  // namespace mmk
