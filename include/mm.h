@@ -140,6 +140,22 @@ int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, vo
  */
 int32_t mm_lambda(double nA, double nB);
 
+/*
+ * mm_winograd_scaled_norms -- mm_winograd_scaled with the two norms supplied by the caller:
+ * norms_device is a DEVICE pointer to {||A||_inf, ||B||_inf} (2 doubles), e.g. the global
+ * ||A||_inf of a row-sharded A after an all-reduce(max) (multi-GPU path).
+ * NULL makes it identical to mm_winograd_scaled.  Same workspace and lambda_out semantics.
+ */
+int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             const double* norms_device, void* workspace, size_t ws_bytes, int32_t* lambda_out,
+                             void* stream);
+
+/*
+ * mm_launch_count -- number of kernels this library has launched in this process (a
+ * monotonically increasing diagnostic counter, used by bench.py's "gpu_launches").
+ */
+uint64_t mm_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

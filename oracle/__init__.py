@@ -84,6 +84,9 @@ def lib() -> ctypes.CDLL:
         L.or_entry_strassen.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, i64, i64, i64, i32,
                                         i64, i64, i64, i64, i64]
         L.or_entry_strassen.restype = d
+        L.or_entries.argtypes = [ctypes.c_int, dp, dp, i64, i64, i64, ip, i64, i32, dp]
+        L.or_entries_strassen.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, i64, i64, i64, i32, i64, i64, i64,
+                                          ip, i64, dp]
         if L.or_selfcheck() != 0:
             raise RuntimeError("oracle self-check failed (contraction or Kahan pin)")
         _lib = L
@@ -278,19 +281,30 @@ def entry(method: int, A, B, i: int, j: int, lam_: int = 0) -> float:
     return float(lib().or_entry(int(method), _dp(A), _dp(B), N, P, M, int(i), int(j), int(lam_)))
 
 
+def _ij(idx) -> np.ndarray:
+    ij = np.ascontiguousarray(np.asarray(idx, dtype=np.int64).reshape(-1, 2))
+    return ij
+
+
 def entries(method: int, A, B, idx, lam_: int = 0) -> np.ndarray:
     A, B, N, P, M = _ab(A, B)
-    L = lib()
-    return np.array([L.or_entry(int(method), _dp(A), _dp(B), N, P, M, int(i), int(j), int(lam_))
-                     for i, j in idx], dtype=np.float64)
+    ij = _ij(idx)
+    if ij.size and (ij[:, 0].min() < 0 or ij[:, 0].max() >= N or ij[:, 1].min() < 0 or ij[:, 1].max() >= M):
+        raise IndexError("entry index out of range")
+    out = np.empty(ij.shape[0], dtype=np.float64)
+    lib().or_entries(int(method), _dp(A), _dp(B), N, P, M, ij.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                     ij.shape[0], int(lam_), _dp(out))
+    return out
 
 
 def entries_strassen(variant: int, A, B, idx, levels=None, pad=None, base: int = BASE_LITERAL) -> np.ndarray:
     A, B, N, P, M = _ab(A, B)
     lv, (Np, Pp, Mp) = _plan(N, P, M, levels, pad)
-    L = lib()
-    return np.array([L.or_entry_strassen(int(variant), int(base), _dp(A), _dp(B), N, P, M, lv, Np, Pp, Mp,
-                                         int(i), int(j)) for i, j in idx], dtype=np.float64)
+    ij = _ij(idx)
+    out = np.empty(ij.shape[0], dtype=np.float64)
+    lib().or_entries_strassen(int(variant), int(base), _dp(A), _dp(B), N, P, M, lv, Np, Pp, Mp,
+                              ij.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ij.shape[0], _dp(out))
+    return out
 
 
 # ---- Brent's bounds; diagnostic formulas, u = 2^-tau -----------

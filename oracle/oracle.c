@@ -646,3 +646,18 @@ double or_entry_strassen(int variant, int base, const double* A, const double* B
   free(cols);
   return r;
 }
+
+/* ------------------------------------------------------------------ batched per-entry calls */
+void or_entries(int method, const double* A, const double* B, int64_t N, int64_t P, int64_t M,
+                const int64_t* ij, int64_t count, int32_t lambda, double* out) {
+  int64_t q;
+  for (q = 0; q < count; q++) out[q] = or_entry(method, A, B, N, P, M, ij[2 * q], ij[2 * q + 1], lambda);
+}
+
+void or_entries_strassen(int variant, int base, const double* A, const double* B, int64_t N, int64_t P,
+                         int64_t M, int32_t levels, int64_t Np, int64_t Pp, int64_t Mp, const int64_t* ij,
+                         int64_t count, double* out) {
+  int64_t q;
+  for (q = 0; q < count; q++)
+    out[q] = or_entry_strassen(variant, base, A, B, N, P, M, levels, Np, Pp, Mp, ij[2 * q], ij[2 * q + 1]);
+}

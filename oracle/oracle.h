@@ -121,6 +121,13 @@ double or_entry_strassen(int variant, int base, const double* A, const double* B
                          int64_t N, int64_t P, int64_t M, int32_t levels,
                          int64_t Np, int64_t Pp, int64_t Mp, int64_t i, int64_t j);
 
+/* the same, over `count` (i, j) pairs stored as ij[2q], ij[2q+1] */
+void or_entries(int method, const double* A, const double* B, int64_t N, int64_t P, int64_t M,
+                const int64_t* ij, int64_t count, int32_t lambda, double* out);
+void or_entries_strassen(int variant, int base, const double* A, const double* B, int64_t N, int64_t P,
+                         int64_t M, int32_t levels, int64_t Np, int64_t Pp, int64_t Mp, const int64_t* ij,
+                         int64_t count, double* out);
+
 #ifdef __cplusplus
 }
 #endif

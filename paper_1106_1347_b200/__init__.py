@@ -37,7 +37,7 @@ METHODS = {
 # every symbol include/mm.h declares
 EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winograd", "mm_winograd_scaled",
            "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
-           "mm_lambda")
+           "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count")
 
 
 class MMError(RuntimeError):
@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         L.norm_inf.argtypes = [dp, i64, i64, dp, vp]
         L.mm_lambda.argtypes = [ctypes.c_double, ctypes.c_double]
         L.mm_lambda.restype = i32
+        L.mm_winograd_scaled_norms.argtypes = [dp, dp, dp, i64, i64, i64, dp, vp, sz, ctypes.POINTER(i32), vp]
+        L.mm_launch_count.restype = ctypes.c_uint64
         _lib = L
     return _lib
 
@@ -187,9 +189,30 @@ def winograd(A, B, *, out=None, stream=None):
     return _gemm(MM_WINOGRAD, "mm_winograd", A, B, out, stream=stream)
 
 
-def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False):
-    """WinogradScaled (PAPER.md:197-217).  return_lambda=True synchronises and returns (C, lambda)."""
-    return _gemm(MM_WINOGRAD_SCALED, "mm_winograd_scaled", A, B, out, stream=stream, want_lambda=return_lambda)
+def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False,
+                    norms: Optional[torch.Tensor] = None):
+    """WinogradScaled (PAPER.md:197-217).  return_lambda=True synchronises and returns (C, lambda).
+    norms: optional 2-element float64 device tensor {||A||_inf, ||B||_inf} (e.g. the global
+    norm of a row-sharded A); default: computed on the device from A and B."""
+    if norms is None:
+        return _gemm(MM_WINOGRAD_SCALED, "mm_winograd_scaled", A, B, out, stream=stream,
+                     want_lambda=return_lambda)
+    N, P, M, out = _operands(A, B, out)
+    if norms.dtype != torch.float64 or norms.numel() != 2 or norms.device != A.device or not norms.is_contiguous():
+        raise ValueError("norms must be a contiguous 2-element float64 tensor on A's device")
+    L = lib()
+    ws_ptr, ws_len = _workspace(int(L.mm_workspace_size(MM_WINOGRAD_SCALED, N, P, M, 0)), A.device)
+    lam = ctypes.c_int32(0)
+    rc = L.mm_winograd_scaled_norms(A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, norms.data_ptr(), ws_ptr,
+                                    ws_len, ctypes.byref(lam) if return_lambda else None,
+                                    _stream_handle(stream, A.device))
+    _check(rc, "mm_winograd_scaled_norms")
+    return (out, int(lam.value)) if return_lambda else out
+
+
+def launch_count() -> int:
+    """Kernels launched by the library so far in this process."""
+    return int(lib().mm_launch_count())
 
 
 def strassen(A, B, *, levels: int = 2, out=None, stream=None):

@@ -3,11 +3,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
 #error "this library is built for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
 #endif
 
 namespace mmk {
+
+// host-side count of kernel launches (mm_launch_count)
+inline std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
 // ---- asynchronous global -> shared copies (LDGSTS).  src_size = 0 zero-fills the
 // destination without reading global memory (used for out-of-range tile elements).

@@ -222,6 +222,7 @@ cudaError_t launch_dgemm_t(const GemmProblem& pr, cudaStream_t st) {
     grid.z = unsigned(cdiv(pr.batch, 65535));
   }
   kern<<<grid, THREADS, smem, st>>>(pr);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -172,6 +172,7 @@ cudaError_t launch_kahan_t(const double* A, const double* B, double* C, int64_t 
   }
   dim3 grid(unsigned(cdiv(M, BN)), unsigned(cdiv(N, BM)));
   kern<<<grid, THREADS, SMEM, st>>>(A, B, C, N, P, M);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -72,6 +72,11 @@ size_t winograd_ws(int64_t N, int64_t M) {
   return mmk::align256(size_t(N) * 8) + mmk::align256(size_t(M) * 8);
 }
 constexpr size_t kScaledHeader = 256;  // norms[2] (u64), scale[2] (double), lambda (int)
+// header | y | z | 2^lambda A | 2^-lambda B
+size_t scaled_ws(int64_t N, int64_t P, int64_t M) {
+  return kScaledHeader + winograd_ws(N, M) + mmk::align256(size_t(N) * size_t(P) * 8) +
+         mmk::align256(size_t(P) * size_t(M) * 8);
+}
 
 }  // namespace
 
@@ -114,7 +119,7 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
     case MM_NAIVE:
     case MM_KAHAN: return 0;
     case MM_WINOGRAD: return winograd_ws(N, M);
-    case MM_WINOGRAD_SCALED: return kScaledHeader + winograd_ws(N, M);
+    case MM_WINOGRAD_SCALED: return scaled_ws(N, P, M);
     case MM_STRASSEN:
     case MM_STRASSEN_WINOGRAD: {
       mmk::StrassenPlan pl;
@@ -134,30 +139,51 @@ int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t 
   if ((rc = check_device(nullptr))) return rc;
   double* y = static_cast<double*>(workspace);
   double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N) * 8));
-  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, mmk::WinogradScale{nullptr}, S(stream)));
+  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, S(stream)));
 }
+
+uint64_t mm_launch_count(void) { return mmk::launch_counter().load(); }
 
 int mm_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                        void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream) {
+  return mm_winograd_scaled_norms(A, B, C, N, P, M, nullptr, workspace, ws_bytes, lambda_out, stream);
+}
+
+int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             const double* norms_device, void* workspace, size_t ws_bytes, int32_t* lambda_out,
+                             void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
-  if (ws_bytes < kScaledHeader + winograd_ws(N, M)) return MM_ERR_WORKSPACE;
-  if ((rc = check_device(nullptr))) return rc;
+  if (ws_bytes < scaled_ws(N, P, M)) return MM_ERR_WORKSPACE;
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
   char* ws = static_cast<char*>(workspace);
   auto* norms = reinterpret_cast<unsigned long long*>(ws);
   auto* scale = reinterpret_cast<double*>(ws + 16);
   auto* lam = reinterpret_cast<int*>(ws + 32);
   double* y = reinterpret_cast<double*>(ws + kScaledHeader);
   double* z = reinterpret_cast<double*>(ws + kScaledHeader + mmk::align256(size_t(N) * 8));
+  double* As = reinterpret_cast<double*>(ws + kScaledHeader + winograd_ws(N, M));
+  double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(P) * 8));
   cudaStream_t st = S(stream);
-  cudaError_t e = mmk::launch_norm_inf(A, N, P, norms, st);
-  if (e == cudaSuccess) e = mmk::launch_norm_inf(B, P, M, norms + 1, st);
+  cudaError_t e = cudaSuccess;
+  const unsigned long long* nrm = norms;
+  if (norms_device) {
+    nrm = reinterpret_cast<const unsigned long long*>(norms_device);  // same 8 bytes, read as bit patterns
+  } else {
+    e = mmk::launch_norm_inf(A, N, P, norms, st);
+    if (e == cudaSuccess) e = mmk::launch_norm_inf(B, P, M, norms + 1, st);
+  }
   if (e == cudaSuccess) {
-    mmk::lambda_kernel<<<1, 32, 0, st>>>(norms, lam, scale);
+    mmk::lambda_kernel<<<1, 32, 0, st>>>(nrm, lam, scale);
+    mmk::note_launch();
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = mmk::launch_winograd(A, B, C, y, z, N, P, M, mmk::WinogradScale{scale}, st);
+  // MultiplyWithScalar: the exact copies 2^lambda A and 2^-lambda B
+  if (e == cudaSuccess) e = mmk::launch_scale_copy(A, As, N * P, scale, 0, sms, st);
+  if (e == cudaSuccess) e = mmk::launch_scale_copy(B, Bs, P * M, scale, 1, sms, st);
+  if (e == cudaSuccess) e = mmk::launch_winograd(As, Bs, C, y, z, N, P, M, st);
   if (e == cudaSuccess && lambda_out) {
     e = cudaMemcpyAsync(lambda_out, lam, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

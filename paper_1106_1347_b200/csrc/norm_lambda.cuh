@@ -100,6 +100,7 @@ inline cudaError_t launch_norm_inf(const double* X, int64_t rows, int64_t cols, 
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   norm_inf_kernel<<<unsigned(cdiv(rows, nrm::ROWS)), nrm::ROWS, 0, st>>>(X, rows, cols, out);
+  note_launch();
   return cudaGetLastError();
 }
 

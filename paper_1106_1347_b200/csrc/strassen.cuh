@@ -270,11 +270,23 @@ cudaError_t launch_form_level(int side, const FormArgs& fa, bool vec, int sms, c
   const int64_t work = fa.cnt * fa.h_rows * (vec ? fa.h_cols / 2 : fa.h_cols);
   const unsigned g = grid_for(work, sms);
   if (side == 0) {
-    if (vec) strassen_form_kernel<VARIANT, 0, 2><<<g, 256, 0, st>>>(fa);
-    else strassen_form_kernel<VARIANT, 0, 1><<<g, 256, 0, st>>>(fa);
+    if (vec) {
+      strassen_form_kernel<VARIANT, 0, 2><<<g, 256, 0, st>>>(fa);
+      note_launch();
+    }
+    else {
+      strassen_form_kernel<VARIANT, 0, 1><<<g, 256, 0, st>>>(fa);
+      note_launch();
+    }
   } else {
-    if (vec) strassen_form_kernel<VARIANT, 1, 2><<<g, 256, 0, st>>>(fa);
-    else strassen_form_kernel<VARIANT, 1, 1><<<g, 256, 0, st>>>(fa);
+    if (vec) {
+      strassen_form_kernel<VARIANT, 1, 2><<<g, 256, 0, st>>>(fa);
+      note_launch();
+    }
+    else {
+      strassen_form_kernel<VARIANT, 1, 1><<<g, 256, 0, st>>>(fa);
+      note_launch();
+    }
   }
   return cudaGetLastError();
 }
@@ -283,8 +295,14 @@ template <int VARIANT>
 cudaError_t launch_combine_level(const CombineArgs& ca, bool vec, int sms, cudaStream_t st) {
   const int64_t work = ca.cnt * ca.h_rows * (vec ? ca.h_cols / 2 : ca.h_cols);
   const unsigned g = grid_for(work, sms);
-  if (vec) strassen_combine_kernel<VARIANT, 2><<<g, 256, 0, st>>>(ca);
-  else strassen_combine_kernel<VARIANT, 1><<<g, 256, 0, st>>>(ca);
+  if (vec) {
+    strassen_combine_kernel<VARIANT, 2><<<g, 256, 0, st>>>(ca);
+    note_launch();
+  }
+  else {
+    strassen_combine_kernel<VARIANT, 1><<<g, 256, 0, st>>>(ca);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

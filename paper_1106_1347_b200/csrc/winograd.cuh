@@ -8,10 +8,9 @@
 // equals the oracle's or_winograd_original bit for bit -- required, because on ill-scaled
 // inputs (config c3) two equally valid summation orders differ by ~50 in the inf-norm.
 //
-// SCALED: the operands are 2^lambda A and 2^-lambda B (exact power-of-two
-// scalings, the oracle's or_scalar_mul), lambda read from device memory written by
-// lambda_kernel, so no host round trip.  Scaling is applied once per staged element in
-// shared memory and in the y/z prologue, never per use.
+// WinogradScaled runs these same kernels on the copies 2^lambda A and
+// 2^-lambda B made by scale_copy_kernel (MultiplyWithScalar; exact power-of-two
+// scalings, lambda read from device memory written by lambda_kernel -- no host round trip).
 //
 // Kernels:
 //  * winograd_yz_kernel: y (one thread per row, A staged through shared memory in
@@ -23,9 +22,24 @@
 
 namespace mmk {
 
-struct WinogradScale {
-  const double* sAB;  // device: [0] = 2^lambda, [1] = 2^-lambda ; nullptr = unscaled
-};
+// MultiplyWithScalar: dst = scale[which] * src, elementwise, HBM-bound.
+__global__ void __launch_bounds__(256) scale_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                         int64_t n, const double* __restrict__ scale, int which) {
+  const double s = scale[which];
+  if ((reinterpret_cast<uintptr_t>(src) & 15) != 0) {  // 8-byte aligned source: scalar path
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+      dst[i] = dmul(s, src[i]);
+    return;
+  }
+  const int64_t n2 = n / 2;
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
+    double2 v = s2[i];
+    d2[i] = make_double2(dmul(s, v.x), dmul(s, v.y));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) dst[n - 1] = dmul(s, src[n - 1]);
+}
 
 // ---------------------------------------------------------------- y / z prologue
 namespace wyz {
@@ -37,14 +51,11 @@ constexpr int TILE_K = 32;    // columns of A staged per step (16 pairs)
 __global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double* __restrict__ A,
                                                                    const double* __restrict__ B,
                                                                    double* __restrict__ y, double* __restrict__ z,
-                                                                   int64_t N, int64_t P, int64_t M, int nb_y,
-                                                                   WinogradScale sc) {
+                                                                   int64_t N, int64_t P, int64_t M, int nb_y) {
   using namespace wyz;
   __shared__ double tileA[THREADS][TILE_K + 1];
   const int tid = threadIdx.x;
   const int64_t gamma = P / 2;
-  const double sa = sc.sAB ? sc.sAB[0] : 1.0;
-  const double sb = sc.sAB ? sc.sAB[1] : 1.0;
   if (int(blockIdx.x) < nb_y) {
     const int64_t r0 = int64_t(blockIdx.x) * THREADS;
     const int64_t kend = 2 * gamma;
@@ -55,9 +66,7 @@ __global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double*
       for (int e = tid; e < THREADS * TILE_K; e += THREADS) {
         const int rr = e / TILE_K, kk = e % TILE_K;
         const int64_t gr = r0 + rr, gk = k0 + kk;
-        double v = (gr < N && gk < kend) ? A[gr * P + gk] : 0.0;
-        if (sc.sAB) v = dmul(sa, v);
-        tileA[rr][kk] = v;
+        tileA[rr][kk] = (gr < N && gk < kend) ? A[gr * P + gk] : 0.0;
       }
       __syncthreads();
       const int64_t rem_k = kend - k0;
@@ -70,14 +79,8 @@ __global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double*
     const int64_t col = int64_t(blockIdx.x - nb_y) * THREADS + tid;
     if (col >= M) return;
     double acc = 0.0;
-    for (int64_t j = 0; j < gamma; ++j) {
-      double b0 = B[(2 * j) * M + col], b1 = B[(2 * j + 1) * M + col];
-      if (sc.sAB) {
-        b0 = dmul(sb, b0);
-        b1 = dmul(sb, b1);
-      }
-      acc = dadd(acc, dmul(b0, b1));
-    }
+#pragma unroll 8
+    for (int64_t j = 0; j < gamma; ++j) acc = dadd(acc, dmul(B[(2 * j) * M + col], B[(2 * j + 1) * M + col]));
     z[col] = acc;
   }
 }
@@ -135,18 +138,10 @@ __device__ __forceinline__ void wino_load_tile(double* As, double* Bs, const dou
   }
 }
 
-// scale, in place, exactly the shared elements this thread copied (after its cp.async completed)
-__device__ __forceinline__ void wino_scale_tile(double* As, double* Bs, double sa, double sb, int tid) {
-  using namespace wino;
-  for (int e = tid; e < A_ELEMS; e += THREADS) As[e] = dmul(sa, As[e]);
-  for (int e = tid; e < B_ELEMS; e += THREADS) Bs[e] = dmul(sb, Bs[e]);
-}
-
-template <int AV, int BV, int CV, bool SCALED>
+template <int AV, int BV, int CV>
 __global__ void __launch_bounds__(wino::THREADS, 1)
     winograd_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                    const double* __restrict__ y, const double* __restrict__ z, int64_t N, int64_t P, int64_t M,
-                    WinogradScale sc) {
+                    const double* __restrict__ y, const double* __restrict__ z, int64_t N, int64_t P, int64_t M) {
   using namespace wino;
   extern __shared__ __align__(128) double smem[];
   double* As_base = smem;
@@ -154,11 +149,6 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
   const int64_t Kend = 2 * (P / 2);
-  double sa = 1.0, sb = 1.0;
-  if (SCALED) {
-    sa = sc.sAB[0];
-    sb = sc.sAB[1];
-  }
 
   double acc[4][8];
 #pragma unroll
@@ -176,13 +166,6 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
   }
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
-    if (SCALED) {
-      // each element was copied by thread (element index % THREADS) in the 8-byte loaders and
-      // by a fixed thread per 16-byte chunk otherwise; a barrier before scaling makes any
-      // element visible to whichever thread scales it.
-      __syncthreads();
-      wino_scale_tile(As_base + (kt % STAGES) * A_ELEMS, Bs_base + (kt % STAGES) * B_ELEMS, sa, sb, tid);
-    }
     __syncthreads();
     {
       const int nk = kt + STAGES - 1;
@@ -228,10 +211,7 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
     if (row >= N) continue;
     const double yi = y[row];
     double alast = 0.0;
-    if (odd) {
-      alast = A[row * P + (P - 1)];
-      if (SCALED) alast = dmul(sa, alast);
-    }
+    if (odd) alast = A[row * P + (P - 1)];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int64_t col = n0 + 2 * tx + 32 * c;
@@ -242,11 +222,7 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
         double v = 0.0;
         if (cc < M) {
           v = dsub(dsub(acc[i][2 * c + e], yi), z[cc]);
-          if (odd) {
-            double blast = B[(P - 1) * M + cc];
-            if (SCALED) blast = dmul(sb, blast);
-            v = dadd(v, dmul(alast, blast));
-          }
+          if (odd) v = dadd(v, dmul(alast, B[(P - 1) * M + cc]));
         }
         out[e] = v;
       }
@@ -260,11 +236,11 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
   }
 }
 
-template <int AV, int BV, int CV, bool SCALED>
+template <int AV, int BV, int CV>
 cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const double* y, const double* z,
-                              int64_t N, int64_t P, int64_t M, WinogradScale sc, cudaStream_t st) {
+                              int64_t N, int64_t P, int64_t M, cudaStream_t st) {
   using namespace wino;
-  auto kern = winograd_kernel<AV, BV, CV, SCALED>;
+  auto kern = winograd_kernel<AV, BV, CV>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
@@ -272,29 +248,34 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
     attr = true;
   }
   dim3 grid(unsigned(cdiv(M, BN)), unsigned(cdiv(N, BM)));
-  kern<<<grid, THREADS, SMEM, st>>>(A, B, C, y, z, N, P, M, sc);
+  kern<<<grid, THREADS, SMEM, st>>>(A, B, C, y, z, N, P, M);
+  note_launch();
   return cudaGetLastError();
 }
 
-// y, z: device buffers of N and M doubles.  sc.sAB == nullptr -> WinogradOriginal.
+// y, z: device buffers of N and M doubles.
 inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
-                                   int64_t P, int64_t M, WinogradScale sc, cudaStream_t st) {
+                                   int64_t P, int64_t M, cudaStream_t st) {
   const int nb_y = int(cdiv(N, wyz::THREADS));
   const int nb_z = int(cdiv(M, wyz::THREADS));
-  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y, sc);
+  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y);
+  note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
-  const bool s = sc.sAB != nullptr;
-  if (av && bv && cv)
-    return s ? launch_winograd_t<2, 2, 2, true>(A, B, C, y, z, N, P, M, sc, st)
-             : launch_winograd_t<2, 2, 2, false>(A, B, C, y, z, N, P, M, sc, st);
-  if (bv && cv)
-    return s ? launch_winograd_t<1, 2, 2, true>(A, B, C, y, z, N, P, M, sc, st)
-             : launch_winograd_t<1, 2, 2, false>(A, B, C, y, z, N, P, M, sc, st);
-  return s ? launch_winograd_t<1, 1, 1, true>(A, B, C, y, z, N, P, M, sc, st)
-           : launch_winograd_t<1, 1, 1, false>(A, B, C, y, z, N, P, M, sc, st);
+  if (av && bv && cv) return launch_winograd_t<2, 2, 2>(A, B, C, y, z, N, P, M, st);
+  if (bv && cv) return launch_winograd_t<1, 2, 2>(A, B, C, y, z, N, P, M, st);
+  return launch_winograd_t<1, 1, 1>(A, B, C, y, z, N, P, M, st);
+}
+
+inline cudaError_t launch_scale_copy(const double* src, double* dst, int64_t n, const double* scale, int which,
+                                     int sms, cudaStream_t st) {
+  int64_t blocks = cdiv(n / 2 + 1, 256);
+  if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
+  scale_copy_kernel<<<unsigned(blocks), 256, 0, st>>>(src, dst, n, scale, which);
+  note_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace mmk

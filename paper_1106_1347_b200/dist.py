@@ -1,0 +1,63 @@
+"""Row-block data parallelism across GPUs (one process per GPU, torch.distributed over NCCL).
+
+C = A B is split by rows: rank r owns rows [r*ceil(N/g), min(N, (r+1)*ceil(N/g))) of A and C
+(workload.shard_rows uses the same rule); B is broadcast from `root` every product -- the one
+real exchange step of the path.  WinogradScaled additionally needs
+the GLOBAL ||A||_inf: each rank's local norm is max-all-reduced (8 bytes), ||B||_inf is local
+because B is replicated, so lambda is identical on every rank and to the 1-GPU run.
+
+Per-entry arithmetic of every kernel depends only on (row of A, column of B, P) -- there is
+no split-K and y_i / z_k are per row / column -- so the classical, Kahan, Winograd and scaled
+Winograd shards are bitwise equal to the corresponding rows of the 1-GPU product.  Strassen on
+a shard recurses on (N_local x P x M) and agrees within its tolerance only.
+
+The compute and norm callables are injectable so that the host-side logic (sharding, the
+broadcast, the max-reduction and lambda) is testable with world_size 2 on CPU (gloo).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(N: int, world: int, rank: int):
+    per = (N + world - 1) // world
+    lo = min(N, rank * per)
+    return lo, min(N, lo + per)
+
+
+def _default_compute(method: str, A, B, out, levels, norms):
+    import paper_1106_1347_b200 as mm
+
+    if method == "winograd_scaled":
+        return mm.winograd_scaled(A, B, out=out, norms=norms)
+    if method in ("strassen", "strassen_winograd"):
+        return getattr(mm, method)(A, B, out=out, levels=levels)
+    return getattr(mm, method)(A, B, out=out)
+
+
+def _default_norm(X):
+    import paper_1106_1347_b200 as mm
+
+    return mm.norm_inf(X)
+
+
+def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None,
+              root: int = 0, group=None, levels: int = 2, compute: Optional[Callable] = None,
+              norm: Optional[Callable] = None) -> torch.Tensor:
+    """C_local = A_local B on every rank.  B must be allocated (P x M) on every rank; its content
+    on `root` is broadcast (in place) before the product.  A rank with no rows still takes part
+    in the collectives and returns an empty (0 x M) result."""
+    compute = compute or _default_compute
+    norm = norm or _default_norm
+    dist.broadcast(B, src=root, group=group)
+    norms = None
+    if method == "winograd_scaled":
+        nA = norm(A_local) if A_local.shape[0] > 0 else torch.zeros(1, dtype=torch.float64, device=B.device)
+        dist.all_reduce(nA, op=dist.ReduceOp.MAX, group=group)  # ||A||_inf = max over row blocks
+        norms = torch.cat([nA.reshape(1), norm(B).reshape(1)])
+    if A_local.shape[0] == 0:
+        return torch.empty((0, B.shape[1]), dtype=B.dtype, device=B.device)
+    return compute(method, A_local, B, out, levels, norms)
