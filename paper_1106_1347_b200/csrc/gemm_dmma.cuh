@@ -2,18 +2,18 @@
 // also the Strassen base case alpha_{m,0}, batched over 7^d products).
 //
 // Design:
-//  * CTA tile 128 x 128 x 16 (doubles), 256 threads = 8 warps in a 2 (M) x 4 (N) grid,
-//    warp tile 64 x 32 = 8 x 4 DMMA.8x8x4 fragments, 64 FP64 accumulators per thread.
+//  * CTA tile BM x BN x 16 doubles, WARPS_M x WARPS_N warps, warp tile (BM/WARPS_M) x
+//    (BN/WARPS_N) made of 8 x 8 DMMA.8x8x4 fragments accumulating in registers.
 //  * Operands staged global -> shared with cp.async (LDGSTS) in a STAGES-deep ring; 16-byte
 //    copies when the operand's rows are 16-byte aligned, else 8-byte copies (e.g. P = 1001).
 //    Out-of-range elements are zero-filled by the copy engine.
 //  * Shared layouts are XOR-swizzled so every fragment load is bank-conflict free:
-//      As[m][k]  at m*16  + (k ^ 4*(m & 3))        (thread (g,t) reads row g, column t)
-//      Bs[k][n]  at k*128 + (n ^ 4*(k & 3))        (thread (g,t) reads row t, column g)
-//  * k is walked in increasing order, 4 per DMMA, accumulating in registers: each C entry
-//    is exactly fma(A_i,P-1 B_P-1,j, ... fma(A_i0 B_0j, 0)) -- the oracle's or_naive_fma.
-//    Tile shape, grid and batch never change that order (no split-K), so sharded and
-//    unsharded runs agree bitwise.
+//      As[m][k]  at m*16 + (k ^ 4*(m & 3))        (thread (g,t) reads row g, column t)
+//      Bs[k][n]  at k*BN + (n ^ 4*(k & 3))        (thread (g,t) reads row t, column g)
+//  * k is walked in increasing order, 4 per DMMA: each C entry is exactly
+//    fma(A[i][P-1], B[P-1][j], ... fma(A[i][0], B[0][j], 0)) -- the oracle's or_naive_fma
+//    (probe P3 established DMMA's chain semantics).  No tile shape, grid or batch changes
+//    that order (no split-K), so sharded and unsharded runs agree bitwise.
 //  * Grid: blockIdx.x = tile id with GROUP_M-row rasterisation for L2 reuse,
 //    blockIdx.y/z = batch index (Strassen's 7^d products).
 #pragma once
@@ -31,83 +31,83 @@ struct GemmProblem {
   int64_t batch;
 };
 
-namespace gemm {
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int WM = 64, WN = 32;
-constexpr int THREADS = 256;
-constexpr int GROUP_M = 8;
-constexpr int A_ELEMS = BM * BK;  // 2048 doubles
-constexpr int B_ELEMS = BK * BN;  // 2048 doubles
-template <int STAGES>
-constexpr size_t smem_bytes() {
-  return size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
-}
-}  // namespace gemm
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = 16;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_, MIN_BLOCKS = MIN_BLOCKS_;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MI = WTM / 8, NJ = WTN / 8;
+  static constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
+  static constexpr int GROUP_M = 8;
+  static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
+  static_assert((A_ELEMS / 2) % THREADS == 0 && (B_ELEMS / 2) % THREADS == 0, "loader split");
+  static_assert(BN % 16 == 0, "B swizzle needs BN % 16 == 0");
+};
 
-template <int AV, int BV>
+// the production configuration: 128 x 64 tiles, 4 warps of 64 x 32, 4 stages, 2 CTAs per SM
+// (tools/tune/gemm_tune.cu compares the alternatives; profiles/r01/gemm_tune*.jsonl).
+// Two independent CTAs per SM let one CTA's barrier/refill overlap the other's DMMAs.
+using GemmDefault = GemmCfg<128, 64, 2, 2, 4, 2>;
+
+template <class CF, int AV, int BV>
 __device__ __forceinline__ void gemm_load_tile(double* As, double* Bs, const double* __restrict__ A,
                                                const double* __restrict__ B, int64_t lda, int64_t ldb, int64_t N,
                                                int64_t P, int64_t M, int64_t m0, int64_t n0, int64_t k0, int tid) {
-  using namespace gemm;
-  // ---- A tile: BM rows x BK k
+  constexpr int BK = CF::BK, BN = CF::BN, T = CF::THREADS;
   if (AV == 2) {
 #pragma unroll
-    for (int i = 0; i < (A_ELEMS / 2) / THREADS; ++i) {  // 4 x 16-byte chunks per thread
-      int c = tid + i * THREADS;
+    for (int i = 0; i < (CF::A_ELEMS / 2) / T; ++i) {
+      int c = tid + i * T;
       int r = c >> 3, kp = (c & 7) * 2;
       int64_t gm = m0 + r, gk = k0 + kp;
       bool v = (gm < N) && (gk < P);
-      const double* src = v ? (A + gm * lda + gk) : A;
-      cp_async16(As + r * BK + (kp ^ ((r & 3) << 2)), src, v);
+      cp_async16(As + r * BK + (kp ^ ((r & 3) << 2)), v ? (A + gm * lda + gk) : A, v);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < A_ELEMS / THREADS; ++i) {  // 8 x 8-byte copies per thread
-      int e = tid + i * THREADS;
+    for (int i = 0; i < CF::A_ELEMS / T; ++i) {
+      int e = tid + i * T;
       int r = e >> 4, kk = e & 15;
       int64_t gm = m0 + r, gk = k0 + kk;
       bool v = (gm < N) && (gk < P);
-      const double* src = v ? (A + gm * lda + gk) : A;
-      cp_async8(As + r * BK + (kk ^ ((r & 3) << 2)), src, v);
+      cp_async8(As + r * BK + (kk ^ ((r & 3) << 2)), v ? (A + gm * lda + gk) : A, v);
     }
   }
-  // ---- B tile: BK k x BN columns
   if (BV == 2) {
 #pragma unroll
-    for (int i = 0; i < (B_ELEMS / 2) / THREADS; ++i) {
-      int c = tid + i * THREADS;
-      int kr = c >> 6, np = (c & 63) * 2;
+    for (int i = 0; i < (CF::B_ELEMS / 2) / T; ++i) {
+      int c = tid + i * T;
+      int kr = c / (BN / 2), np = (c % (BN / 2)) * 2;
       int64_t gk = k0 + kr, gn = n0 + np;
       bool v = (gk < P) && (gn < M);
-      const double* src = v ? (B + gk * ldb + gn) : B;
-      cp_async16(Bs + kr * BN + (np ^ ((kr & 3) << 2)), src, v);
+      cp_async16(Bs + kr * BN + (np ^ ((kr & 3) << 2)), v ? (B + gk * ldb + gn) : B, v);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < B_ELEMS / THREADS; ++i) {
-      int e = tid + i * THREADS;
-      int kr = e >> 7, nn = e & 127;
+    for (int i = 0; i < CF::B_ELEMS / T; ++i) {
+      int e = tid + i * T;
+      int kr = e / BN, nn = e % BN;
       int64_t gk = k0 + kr, gn = n0 + nn;
       bool v = (gk < P) && (gn < M);
-      const double* src = v ? (B + gk * ldb + gn) : B;
-      cp_async8(Bs + kr * BN + (nn ^ ((kr & 3) << 2)), src, v);
+      cp_async8(Bs + kr * BN + (nn ^ ((kr & 3) << 2)), v ? (B + gk * ldb + gn) : B, v);
     }
   }
 }
 
-template <int AV, int BV, int CV, int STAGES>
-__global__ void __launch_bounds__(gemm::THREADS, 1) dgemm_dmma_kernel(GemmProblem pr) {
-  using namespace gemm;
+template <class CF, int AV, int BV, int CV>
+__global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_dmma_kernel(GemmProblem pr) {
+  constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES, MI = CF::MI, NJ = CF::NJ;
   extern __shared__ __align__(128) double smem[];
   double* As_base = smem;
-  double* Bs_base = smem + STAGES * A_ELEMS;
+  double* Bs_base = smem + STAGES * CF::A_ELEMS;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / CF::WARPS_N, wn = warp % CF::WARPS_N;
 
-  // ---- batch and tile coordinates
   const int64_t bidx = int64_t(blockIdx.y) + int64_t(gridDim.y) * blockIdx.z;
   if (bidx >= pr.batch) return;
   const double* __restrict__ A = pr.A + bidx * pr.sA;
@@ -115,34 +115,30 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) dgemm_dmma_kernel(GemmProble
   double* __restrict__ C = pr.C + bidx * pr.sC;
   const int tiles_m = int(cdiv(pr.N, BM)), tiles_n = int(cdiv(pr.M, BN));
   const int tile = blockIdx.x;
-  const int group = tile / (GROUP_M * tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gsize = min(tiles_m - first_m, GROUP_M);
-  const int in_group = tile - group * GROUP_M * tiles_n;
-  const int tm = first_m + in_group % gsize;
-  const int tn = in_group / gsize;
-  const int64_t m0 = int64_t(tm) * BM, n0 = int64_t(tn) * BN;
+  const int group = tile / (CF::GROUP_M * tiles_n);
+  const int first_m = group * CF::GROUP_M;
+  const int gsize = min(tiles_m - first_m, CF::GROUP_M);
+  const int in_group = tile - group * CF::GROUP_M * tiles_n;
+  const int64_t m0 = int64_t(first_m + in_group % gsize) * BM, n0 = int64_t(in_group / gsize) * BN;
 
-  double acc[8][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int KT = int(cdiv(pr.P, BK));
-
-  // ---- prologue: fill STAGES-1 stages
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT)
-      gemm_load_tile<AV, BV>(As_base + s * A_ELEMS, Bs_base + s * B_ELEMS, A, B, pr.lda, pr.ldb, pr.N, pr.P, pr.M,
-                             m0, n0, int64_t(s) * BK, tid);
+      gemm_load_tile<CF, AV, BV>(As_base + s * CF::A_ELEMS, Bs_base + s * CF::B_ELEMS, A, B, pr.lda, pr.ldb, pr.N,
+                                 pr.P, pr.M, m0, n0, int64_t(s) * BK, tid);
     cp_async_commit();
   }
 
-  // per-thread fragment offsets inside a stage
-  const int a_row0 = wm * WM + g;  // + 8*mi
-  const int b_col0 = wn * WN + g;  // + 8*nj
+  const int a_row0 = wm * CF::WTM + g;  // + 8*mi ; (a_row0 + 8 mi) & 3 == g & 3
+  const int b_col0 = wn * CF::WTN + g;  // + 8*nj
+  const int a_sw = (g & 3) << 2, b_sw = t << 2;
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
@@ -151,44 +147,37 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) dgemm_dmma_kernel(GemmProble
       const int nk = kt + STAGES - 1;
       if (nk < KT) {
         const int s = nk % STAGES;
-        gemm_load_tile<AV, BV>(As_base + s * A_ELEMS, Bs_base + s * B_ELEMS, A, B, pr.lda, pr.ldb, pr.N, pr.P,
-                               pr.M, m0, n0, int64_t(nk) * BK, tid);
+        gemm_load_tile<CF, AV, BV>(As_base + s * CF::A_ELEMS, Bs_base + s * CF::B_ELEMS, A, B, pr.lda, pr.ldb,
+                                   pr.N, pr.P, pr.M, m0, n0, int64_t(nk) * BK, tid);
       }
       cp_async_commit();
     }
-    const double* As = As_base + (kt % STAGES) * A_ELEMS;
-    const double* Bs = Bs_base + (kt % STAGES) * B_ELEMS;
+    const double* As = As_base + (kt % STAGES) * CF::A_ELEMS;
+    const double* Bs = Bs_base + (kt % STAGES) * CF::B_ELEMS;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       const int k = ks * 4 + t;
-      double af[8], bf[4];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const int r = a_row0 + 8 * mi;  // r & 3 == g & 3
-        af[mi] = As[r * BK + (k ^ ((g & 3) << 2))];
-      }
+      for (int mi = 0; mi < MI; ++mi) af[mi] = As[(a_row0 + 8 * mi) * BK + (k ^ a_sw)];
 #pragma unroll
-      for (int nj = 0; nj < 4; ++nj) {
-        const int c = b_col0 + 8 * nj;
-        bf[nj] = Bs[k * BN + (c ^ (t << 2))];  // k & 3 == t
-      }
+      for (int nj = 0; nj < NJ; ++nj) bf[nj] = Bs[k * BN + ((b_col0 + 8 * nj) ^ b_sw)];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
+        for (int nj = 0; nj < NJ; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
     }
   }
   cp_async_wait<0>();
 
-  // ---- epilogue: registers -> global
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
+  for (int mi = 0; mi < MI; ++mi) {
     const int64_t row = m0 + a_row0 + 8 * mi;
     if (row >= pr.N) continue;
     double* crow = C + row * pr.ldc;
 #pragma unroll
-    for (int nj = 0; nj < 4; ++nj) {
-      const int64_t col = n0 + b_col0 - g + 8 * nj + 2 * t;
+    for (int nj = 0; nj < NJ; ++nj) {
+      const int64_t col = n0 + wn * CF::WTN + 8 * nj + 2 * t;
       if (CV == 2 && col + 1 < pr.M) {
         *reinterpret_cast<double2*>(crow + col) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
       } else {
@@ -200,20 +189,16 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) dgemm_dmma_kernel(GemmProble
 }
 
 // ---- host-side launcher ------------------------------------------------------
-constexpr int GEMM_STAGES = 4;
-
-template <int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV>
 cudaError_t launch_dgemm_t(const GemmProblem& pr, cudaStream_t st) {
-  using namespace gemm;
-  auto kern = dgemm_dmma_kernel<AV, BV, CV, GEMM_STAGES>;
-  const size_t smem = smem_bytes<GEMM_STAGES>();
+  auto kern = dgemm_dmma_kernel<CF, AV, BV, CV>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int64_t tiles = cdiv(pr.N, BM) * cdiv(pr.M, BN);
+  const int64_t tiles = cdiv(pr.N, CF::BM) * cdiv(pr.M, CF::BN);
   dim3 grid(unsigned(tiles), 1, 1);
   if (pr.batch <= 65535) {
     grid.y = unsigned(pr.batch);
@@ -221,7 +206,7 @@ cudaError_t launch_dgemm_t(const GemmProblem& pr, cudaStream_t st) {
     grid.y = 65535;
     grid.z = unsigned(cdiv(pr.batch, 65535));
   }
-  kern<<<grid, THREADS, smem, st>>>(pr);
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(pr);
   note_launch();
   return cudaGetLastError();
 }
@@ -229,18 +214,19 @@ cudaError_t launch_dgemm_t(const GemmProblem& pr, cudaStream_t st) {
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // chooses the 16-byte or 8-byte loaders per operand
+template <class CF = GemmDefault>
 inline cudaError_t launch_dgemm(const GemmProblem& pr, cudaStream_t st) {
   const bool av = aligned16(pr.A) && (pr.lda % 2 == 0) && (pr.batch == 1 || pr.sA % 2 == 0);
   const bool bv = aligned16(pr.B) && (pr.ldb % 2 == 0) && (pr.batch == 1 || pr.sB % 2 == 0);
   const bool cv = aligned16(pr.C) && (pr.ldc % 2 == 0) && (pr.batch == 1 || pr.sC % 2 == 0);
-  if (av && bv && cv) return launch_dgemm_t<2, 2, 2>(pr, st);
-  if (av && bv) return launch_dgemm_t<2, 2, 1>(pr, st);
-  if (av && cv) return launch_dgemm_t<2, 1, 2>(pr, st);
-  if (bv && cv) return launch_dgemm_t<1, 2, 2>(pr, st);
-  if (av) return launch_dgemm_t<2, 1, 1>(pr, st);
-  if (bv) return launch_dgemm_t<1, 2, 1>(pr, st);
-  if (cv) return launch_dgemm_t<1, 1, 2>(pr, st);
-  return launch_dgemm_t<1, 1, 1>(pr, st);
+  if (av && bv && cv) return launch_dgemm_t<CF, 2, 2, 2>(pr, st);
+  if (av && bv) return launch_dgemm_t<CF, 2, 2, 1>(pr, st);
+  if (av && cv) return launch_dgemm_t<CF, 2, 1, 2>(pr, st);
+  if (bv && cv) return launch_dgemm_t<CF, 1, 2, 2>(pr, st);
+  if (av) return launch_dgemm_t<CF, 2, 1, 1>(pr, st);
+  if (bv) return launch_dgemm_t<CF, 1, 2, 1>(pr, st);
+  if (cv) return launch_dgemm_t<CF, 1, 1, 2>(pr, st);
+  return launch_dgemm_t<CF, 1, 1, 1>(pr, st);
 }
 
 }  // namespace mmk

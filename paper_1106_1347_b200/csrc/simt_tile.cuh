@@ -1,0 +1,66 @@
+// simt_tile.cuh -- tile configuration and cp.async tile loader shared by the FP64 SIMT
+// kernels (K2 Kahan, K3 Winograd).  Product path only.
+#pragma once
+#include "common.cuh"
+
+namespace mmk {
+
+// CTA tile BM x BN x 16, thread tile TM x TN, STAGES-deep cp.async ring, MINB CTAs per SM.
+template <int BM_, int BN_, int TM_, int TN_, int STAGES_, int MINB_>
+struct SimtCfg {
+  static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BK = 16, APITCH = BK + 2;
+  static constexpr int TXN = BN / TN, TYM = BM / TM, THREADS = TXN * TYM;
+  static constexpr int A_ELEMS = BM * APITCH, B_ELEMS = BK * BN;
+  static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
+  static_assert(TN % 2 == 0, "columns are handled in pairs");
+  static_assert((BM * BK / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0, "loader split");
+};
+
+// A tile (BM x BK, rows padded to APITCH) and B tile (BK x BN); `kend` bounds k (zero fill past it)
+template <class CF, int AV, int BV>
+__device__ __forceinline__ void simt_load_tile(double* As, double* Bs, const double* __restrict__ A,
+                                               const double* __restrict__ B, int64_t N, int64_t P, int64_t M,
+                                               int64_t kend, int64_t m0, int64_t n0, int64_t k0, int tid) {
+  constexpr int BK = CF::BK, BN = CF::BN, T = CF::THREADS, AP = CF::APITCH;
+  if (AV == 2) {
+#pragma unroll
+    for (int i = 0; i < (CF::BM * BK / 2) / T; ++i) {
+      int c = tid + i * T;
+      int r = c >> 3, kp = (c & 7) * 2;
+      int64_t gm = m0 + r, gk = k0 + kp;
+      bool v = gm < N && gk < kend;
+      cp_async16(As + r * AP + kp, v ? A + gm * P + gk : A, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < (CF::BM * BK) / T; ++i) {
+      int e = tid + i * T;
+      int r = e >> 4, kk = e & 15;
+      int64_t gm = m0 + r, gk = k0 + kk;
+      bool v = gm < N && gk < kend;
+      cp_async8(As + r * AP + kk, v ? A + gm * P + gk : A, v);
+    }
+  }
+  if (BV == 2) {
+#pragma unroll
+    for (int i = 0; i < (BK * BN / 2) / T; ++i) {
+      int c = tid + i * T;
+      int kr = c / (BN / 2), np = (c % (BN / 2)) * 2;
+      int64_t gk = k0 + kr, gn = n0 + np;
+      bool v = gk < kend && gn < M;
+      cp_async16(Bs + kr * BN + np, v ? B + gk * M + gn : B, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < (BK * BN) / T; ++i) {
+      int e = tid + i * T;
+      int kr = e / BN, nn = e % BN;
+      int64_t gk = k0 + kr, gn = n0 + nn;
+      bool v = gk < kend && gn < M;
+      cp_async8(Bs + kr * BN + nn, v ? B + gk * M + gn : B, v);
+    }
+  }
+}
+
+}  // namespace mmk

@@ -18,7 +18,7 @@
 //  * winograd_kernel: CTA 64 x 128, 256 threads, 4 x 8 outputs per thread; the pair loop
 //    covers columns 0..2*gamma-1 only (the odd column never enters acc).
 #pragma once
-#include "common.cuh"
+#include "simt_tile.cuh"
 
 namespace mmk {
 
@@ -86,82 +86,35 @@ __global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double*
 }
 
 // ---------------------------------------------------------------- main pair-sum kernel
-namespace wino {
-constexpr int BM = 64, BN = 128, BK = 16, THREADS = 256, STAGES = 3;
-constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
-constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
-}  // namespace wino
+using WinogradDefault = SimtCfg<64, 128, 4, 8, 3, 1>;
 
-// Kend = 2*gamma: columns/rows >= Kend are zero-filled (the odd column is excluded).
-template <int AV, int BV>
-__device__ __forceinline__ void wino_load_tile(double* As, double* Bs, const double* __restrict__ A,
-                                               const double* __restrict__ B, int64_t N, int64_t P, int64_t M,
-                                               int64_t Kend, int64_t m0, int64_t n0, int64_t k0, int tid) {
-  using namespace wino;
-  if (AV == 2) {
-#pragma unroll
-    for (int i = 0; i < (A_ELEMS / 2) / THREADS; ++i) {
-      int c = tid + i * THREADS;
-      int r = c >> 3, kp = (c & 7) * 2;
-      int64_t gm = m0 + r, gk = k0 + kp;
-      bool v = gm < N && gk < Kend;
-      cp_async16(As + r * BK + kp, v ? A + gm * P + gk : A, v);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < A_ELEMS / THREADS; ++i) {
-      int e = tid + i * THREADS;
-      int r = e >> 4, kk = e & 15;
-      int64_t gm = m0 + r, gk = k0 + kk;
-      bool v = gm < N && gk < Kend;
-      cp_async8(As + r * BK + kk, v ? A + gm * P + gk : A, v);
-    }
-  }
-  if (BV == 2) {
-#pragma unroll
-    for (int i = 0; i < (B_ELEMS / 2) / THREADS; ++i) {
-      int c = tid + i * THREADS;
-      int kr = c >> 6, np = (c & 63) * 2;
-      int64_t gk = k0 + kr, gn = n0 + np;
-      bool v = gk < Kend && gn < M;
-      cp_async16(Bs + kr * BN + np, v ? B + gk * M + gn : B, v);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < B_ELEMS / THREADS; ++i) {
-      int e = tid + i * THREADS;
-      int kr = e >> 7, nn = e & 127;
-      int64_t gk = k0 + kr, gn = n0 + nn;
-      bool v = gk < Kend && gn < M;
-      cp_async8(Bs + kr * BN + nn, v ? B + gk * M + gn : B, v);
-    }
-  }
-}
-
-template <int AV, int BV, int CV>
-__global__ void __launch_bounds__(wino::THREADS, 1)
+// The tiles are loaded with kend = 2*gamma: columns/rows >= 2*gamma are zero-filled, so the
+// odd column never enters acc.  A zero-filled pair adds (0+0)(0+0) = +0 to acc, which leaves
+// acc unchanged (acc starts at +0 and can never become -0), so the last tile needs no guard.
+template <class CF, int AV, int BV, int CV>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     winograd_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                     const double* __restrict__ y, const double* __restrict__ z, int64_t N, int64_t P, int64_t M) {
-  using namespace wino;
+  constexpr int BK = CF::BK, STAGES = CF::STAGES, TM = CF::TM, TN = CF::TN;
   extern __shared__ __align__(128) double smem[];
   double* As_base = smem;
-  double* Bs_base = smem + STAGES * A_ELEMS;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  double* Bs_base = smem + STAGES * CF::A_ELEMS;
+  const int tid = threadIdx.x, tx = tid % CF::TXN, ty = tid / CF::TXN;
+  const int64_t m0 = int64_t(blockIdx.y) * CF::BM, n0 = int64_t(blockIdx.x) * CF::BN;
   const int64_t Kend = 2 * (P / 2);
 
-  double acc[4][8];
+  double acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
 
   const int KT = int(cdiv(Kend, BK));
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
     if (st < KT)
-      wino_load_tile<AV, BV>(As_base + st * A_ELEMS, Bs_base + st * B_ELEMS, A, B, N, P, M, Kend, m0, n0,
-                             int64_t(st) * BK, tid);
+      simt_load_tile<CF, AV, BV>(As_base + st * CF::A_ELEMS, Bs_base + st * CF::B_ELEMS, A, B, N, P, M, Kend, m0,
+                                 n0, int64_t(st) * BK, tid);
     cp_async_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
@@ -170,59 +123,56 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
     {
       const int nk = kt + STAGES - 1;
       if (nk < KT)
-        wino_load_tile<AV, BV>(As_base + (nk % STAGES) * A_ELEMS, Bs_base + (nk % STAGES) * B_ELEMS, A, B, N, P, M,
-                               Kend, m0, n0, int64_t(nk) * BK, tid);
+        simt_load_tile<CF, AV, BV>(As_base + (nk % STAGES) * CF::A_ELEMS, Bs_base + (nk % STAGES) * CF::B_ELEMS, A,
+                                   B, N, P, M, Kend, m0, n0, int64_t(nk) * BK, tid);
       cp_async_commit();
     }
-    const double* As = As_base + (kt % STAGES) * A_ELEMS;
-    const double* Bs = Bs_base + (kt % STAGES) * B_ELEMS;
-    // zero-filled pairs past Kend add (0+0)(0+0) = +0 to acc, which leaves acc unchanged
-    // (acc starts at +0 and can never become -0), so the last tile needs no guard.
+    const double* As = As_base + (kt % STAGES) * CF::A_ELEMS;
+    const double* Bs = Bs_base + (kt % STAGES) * CF::B_ELEMS;
 #pragma unroll 2
     for (int jp = 0; jp < BK / 2; ++jp) {
-      double a0[4], a1[4], b0[8], b1[8];
+      double a0[TM], a1[TM], b0[TN], b1[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double2 v = *reinterpret_cast<const double2*>(As + (4 * ty + i) * BK + 2 * jp);
+      for (int i = 0; i < TM; ++i) {
+        double2 v = *reinterpret_cast<const double2*>(As + (TM * ty + i) * CF::APITCH + 2 * jp);
         a0[i] = v.x;
         a1[i] = v.y;
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double2 u = *reinterpret_cast<const double2*>(Bs + (2 * jp) * BN + 2 * tx + 32 * c);
-        double2 w = *reinterpret_cast<const double2*>(Bs + (2 * jp + 1) * BN + 2 * tx + 32 * c);
+      for (int c = 0; c < TN / 2; ++c) {
+        double2 u = *reinterpret_cast<const double2*>(Bs + (2 * jp) * CF::BN + 2 * tx + 2 * CF::TXN * c);
+        double2 w = *reinterpret_cast<const double2*>(Bs + (2 * jp + 1) * CF::BN + 2 * tx + 2 * CF::TXN * c);
         b0[2 * c] = u.x;
         b0[2 * c + 1] = u.y;
         b1[2 * c] = w.x;
         b1[2 * c + 1] = w.y;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
+        for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
     }
   }
   cp_async_wait<0>();
 
   const bool odd = (P & 1) != 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = m0 + 4 * ty + i;
+  for (int i = 0; i < TM; ++i) {
+    const int64_t row = m0 + TM * ty + i;
     if (row >= N) continue;
     const double yi = y[row];
-    double alast = 0.0;
-    if (odd) alast = A[row * P + (P - 1)];
+    const double alast = odd ? A[row * P + (P - 1)] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int64_t col = n0 + 2 * tx + 32 * c;
+    for (int c = 0; c < TN / 2; ++c) {
+      const int64_t col = n0 + 2 * tx + 2 * CF::TXN * c;
       double out[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t cc = col + e;
         double v = 0.0;
         if (cc < M) {
-          v = dsub(dsub(acc[i][2 * c + e], yi), z[cc]);
-          if (odd) v = dadd(v, dmul(alast, B[(P - 1) * M + cc]));
+          v = dsub(dsub(acc[i][2 * c + e], yi), z[cc]);             // (acc - y_i) - z_k
+          if (odd) v = dadd(v, dmul(alast, B[(P - 1) * M + cc]));   // + A_{i,P} B_{P,k}
         }
         out[e] = v;
       }
@@ -236,37 +186,42 @@ __global__ void __launch_bounds__(wino::THREADS, 1)
   }
 }
 
-template <int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV>
 cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const double* y, const double* z,
                               int64_t N, int64_t P, int64_t M, cudaStream_t st) {
-  using namespace wino;
-  auto kern = winograd_kernel<AV, BV, CV>;
+  auto kern = winograd_kernel<CF, AV, BV, CV>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(unsigned(cdiv(M, BN)), unsigned(cdiv(N, BM)));
-  kern<<<grid, THREADS, SMEM, st>>>(A, B, C, y, z, N, P, M);
+  dim3 grid(unsigned(cdiv(M, CF::BN)), unsigned(cdiv(N, CF::BM)));
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(A, B, C, y, z, N, P, M);
+  note_launch();
+  return cudaGetLastError();
+}
+
+inline cudaError_t launch_winograd_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P,
+                                      int64_t M, cudaStream_t st) {
+  const int nb_y = int(cdiv(N, wyz::THREADS));
+  const int nb_z = int(cdiv(M, wyz::THREADS));
+  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y);
   note_launch();
   return cudaGetLastError();
 }
 
 // y, z: device buffers of N and M doubles.
+template <class CF = WinogradDefault>
 inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
                                    int64_t P, int64_t M, cudaStream_t st) {
-  const int nb_y = int(cdiv(N, wyz::THREADS));
-  const int nb_z = int(cdiv(M, wyz::THREADS));
-  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_winograd_yz(A, B, y, z, N, P, M, st);
   if (e != cudaSuccess) return e;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
-  if (av && bv && cv) return launch_winograd_t<2, 2, 2>(A, B, C, y, z, N, P, M, st);
-  if (bv && cv) return launch_winograd_t<1, 2, 2>(A, B, C, y, z, N, P, M, st);
-  return launch_winograd_t<1, 1, 1>(A, B, C, y, z, N, P, M, st);
+  if (av && bv && cv) return launch_winograd_t<CF, 2, 2, 2>(A, B, C, y, z, N, P, M, st);
+  if (bv && cv) return launch_winograd_t<CF, 1, 2, 2>(A, B, C, y, z, N, P, M, st);
+  return launch_winograd_t<CF, 1, 1, 1>(A, B, C, y, z, N, P, M, st);
 }
 
 inline cudaError_t launch_scale_copy(const double* src, double* dst, int64_t n, const double* scale, int which,

@@ -1,0 +1,83 @@
+// gemm_tune.cu -- development harness: times alternative K1 tile configurations on B200 and
+// checks they are bitwise identical (they all walk k in the same order).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o gemm_tune gemm_tune.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../paper_1106_1347_b200/csrc/gemm_dmma.cuh"
+
+using namespace mmk;
+
+__global__ void fill(double* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i] = double(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+  }
+}
+
+__global__ void cmp(const double* a, const double* b, int64_t n, unsigned long long* bad) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    if (a[i] != b[i]) atomicAdd(bad, 1ull);
+}
+
+template <class CF>
+void run(const char* name, const double* A, const double* B, double* C, const double* Cref, int64_t n, int reps,
+         unsigned long long* bad) {
+  GemmProblem pr{A, B, C, n, n, n, n, n, n, 0, 0, 0, 1};
+  cudaMemset(C, 0, n * n * 8);
+  if (launch_dgemm<CF>(pr, 0) != cudaSuccess) {
+    printf("{\"cfg\":\"%s\",\"error\":\"%s\"}\n", name, cudaGetErrorString(cudaGetLastError()));
+    return;
+  }
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) launch_dgemm<CF>(pr, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  unsigned long long nb = 0;
+  if (Cref) {
+    cudaMemset(bad, 0, 8);
+    cmp<<<1024, 256>>>(C, Cref, n * n, bad);
+    cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
+  }
+  cudaError_t err = cudaGetLastError();
+  printf("{\"cfg\":\"%s\",\"n\":%lld,\"threads\":%d,\"smem\":%zu,\"ms\":%.3f,\"tflops\":%.2f,\"mismatch\":%llu,\"err\":\"%s\"}\n",
+         name, (long long)n, CF::THREADS, CF::SMEM, ms, 2.0 * n * n * n / ms / 1e9, nb, cudaGetErrorString(err));
+  fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+  int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
+  int reps = argc > 2 ? atoi(argv[2]) : 3;
+  double *A, *B, *C, *R;
+  unsigned long long* bad;
+  cudaMalloc(&A, n * n * 8);
+  cudaMalloc(&B, n * n * 8);
+  cudaMalloc(&C, n * n * 8);
+  cudaMalloc(&R, n * n * 8);
+  cudaMalloc(&bad, 8);
+  fill<<<1024, 256>>>(A, n * n, 1);
+  fill<<<1024, 256>>>(B, n * n, 2);
+  run<GemmCfg<128, 64, 2, 2, 4, 2>>("128x64_w2x2_s4_2cta", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<128, 64, 2, 2, 3, 2>>("128x64_w2x2_s3_2cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 128, 1, 4, 4, 2>>("64x128_w1x4_s4_2cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 128, 1, 4, 3, 2>>("64x128_w1x4_s3_2cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 128, 2, 2, 4, 2>>("64x128_w2x2_s4_2cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 1, 2, 3, 4>>("64x64_w1x2_s3_4cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 1, 2, 2, 4>>("64x64_w1x2_s2_4cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 32, 2, 1, 4, 3>>("128x32_w2x1_s4_3cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 4>>("64x64_w2x2_s4_4cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 3, 5>>("64x64_w2x2_s3_5cta", A, B, C, R, n, reps, bad);
+  return 0;
+}

@@ -1,0 +1,109 @@
+// simt_tune.cu -- development harness: times alternative tile configurations of the FP64
+// SIMT kernels (K2 Kahan, K3 Winograd) on B200 and checks that each is bitwise identical to
+// the first (every configuration walks k / j in the same order per entry).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o simt_tune simt_tune.cu
+#include <cstdio>
+#include <cstdlib>
+
+#include "../../paper_1106_1347_b200/csrc/kahan.cuh"
+#include "../../paper_1106_1347_b200/csrc/winograd.cuh"
+
+using namespace mmk;
+
+__global__ void fill(double* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i] = double(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+  }
+}
+
+__global__ void cmp(const double* a, const double* b, int64_t n, unsigned long long* bad) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    if (a[i] != b[i]) atomicAdd(bad, 1ull);
+}
+
+struct Ctx {
+  double *A, *B, *C, *R, *y, *z;
+  unsigned long long* bad;
+  int64_t n;
+  int reps;
+};
+
+template <class F>
+void timeit(const char* kind, const char* name, int threads, size_t smem, Ctx& c, const double* ref, F f,
+            double ops_per_entry_k) {
+  cudaMemset(c.C, 0, c.n * c.n * 8);
+  f();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < c.reps; ++r) f();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= c.reps;
+  unsigned long long nb = 0;
+  if (ref) {
+    cudaMemset(c.bad, 0, 8);
+    cmp<<<1024, 256>>>(c.C, ref, c.n * c.n, c.bad);
+    cudaMemcpy(&nb, c.bad, 8, cudaMemcpyDeviceToHost);
+  }
+  const double n = double(c.n);
+  printf("{\"kernel\":\"%s\",\"cfg\":\"%s\",\"n\":%lld,\"threads\":%d,\"smem\":%zu,\"ms\":%.3f,\"gflops_2npm\":%.1f,"
+         "\"fp64_op_rate_T\":%.3f,\"mismatch\":%llu,\"err\":\"%s\"}\n",
+         kind, name, (long long)c.n, threads, smem, ms, 2 * n * n * n / ms / 1e6, ops_per_entry_k * n * n * n / ms / 1e9,
+         nb, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
+template <class CF>
+void kahan(const char* name, Ctx& c, bool first) {
+  if (first) cudaMemset(c.R, 0, c.n * c.n * 8);
+  timeit("kahan", name, CF::THREADS, CF::SMEM, c, first ? nullptr : c.R,
+         [&] { launch_kahan<CF>(c.A, c.B, c.C, c.n, c.n, c.n, 0); }, 5.0);
+  if (first) cudaMemcpy(c.R, c.C, c.n * c.n * 8, cudaMemcpyDeviceToDevice);
+}
+
+template <class CF>
+void wino(const char* name, Ctx& c, bool first) {
+  timeit("winograd", name, CF::THREADS, CF::SMEM, c, first ? nullptr : c.R,
+         [&] { launch_winograd<CF>(c.A, c.B, c.C, c.y, c.z, c.n, c.n, c.n, 0); }, 2.0);
+  if (first) cudaMemcpy(c.R, c.C, c.n * c.n * 8, cudaMemcpyDeviceToDevice);
+}
+
+int main(int argc, char** argv) {
+  Ctx c;
+  c.n = argc > 1 ? atoll(argv[1]) : 8192;
+  c.reps = argc > 2 ? atoi(argv[2]) : 2;
+  cudaMalloc(&c.A, c.n * c.n * 8);
+  cudaMalloc(&c.B, c.n * c.n * 8);
+  cudaMalloc(&c.C, c.n * c.n * 8);
+  cudaMalloc(&c.R, c.n * c.n * 8);
+  cudaMalloc(&c.y, c.n * 8);
+  cudaMalloc(&c.z, c.n * 8);
+  cudaMalloc(&c.bad, 8);
+  fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
+  fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
+  // SimtCfg<BM, BN, TM, TN, STAGES, MINB>
+  wino<SimtCfg<64, 128, 4, 8, 3, 1>>("64x128_t4x8_s3", c, true);
+  wino<SimtCfg<64, 64, 4, 4, 3, 2>>("64x64_t4x4_s3_2cta", c, false);
+  wino<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, false);
+  wino<SimtCfg<32, 128, 4, 8, 3, 2>>("32x128_t4x8_s3_2cta", c, false);
+  wino<SimtCfg<64, 128, 4, 4, 3, 1>>("64x128_t4x4_s3", c, false);
+  wino<SimtCfg<128, 128, 8, 8, 3, 1>>("128x128_t8x8_s3", c, false);
+  wino<SimtCfg<128, 64, 8, 4, 3, 2>>("128x64_t8x4_s3_2cta", c, false);
+  wino<SimtCfg<64, 64, 4, 4, 2, 3>>("64x64_t4x4_s2_3cta", c, false);
+  kahan<SimtCfg<64, 128, 4, 8, 3, 1>>("64x128_t4x8_s3", c, true);
+  kahan<SimtCfg<64, 64, 4, 4, 3, 2>>("64x64_t4x4_s3_2cta", c, false);
+  kahan<SimtCfg<32, 128, 4, 8, 3, 2>>("32x128_t4x8_s3_2cta", c, false);
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, false);
+  kahan<SimtCfg<64, 128, 4, 4, 3, 1>>("64x128_t4x4_s3", c, false);
+  kahan<SimtCfg<64, 64, 4, 4, 2, 3>>("64x64_t4x4_s2_3cta", c, false);
+  return 0;
+}
