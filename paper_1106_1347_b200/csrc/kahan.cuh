@@ -16,7 +16,8 @@
 
 namespace mmk {
 
-using KahanDefault = SimtCfg<64, 128, 4, 8, 3, 1>;
+// 64 x 64 tiles, 128 threads of 4 x 8 outputs, 2 CTAs per SM (tools/tune/simt_tune.cu)
+using KahanDefault = SimtCfg<64, 64, 4, 8, 3, 2>;
 
 template <class CF>
 __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double (&err)[CF::TM][CF::TN],

@@ -136,10 +136,11 @@ int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t 
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
   if (ws_bytes < winograd_ws(N, M)) return MM_ERR_WORKSPACE;
-  if ((rc = check_device(nullptr))) return rc;
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
   double* y = static_cast<double*>(workspace);
   double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N) * 8));
-  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, S(stream)));
+  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, S(stream), sms));
 }
 
 uint64_t mm_launch_count(void) { return mmk::launch_counter().load(); }
@@ -183,7 +184,7 @@ int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_
   // MultiplyWithScalar: the exact copies 2^lambda A and 2^-lambda B
   if (e == cudaSuccess) e = mmk::launch_scale_copy(A, As, N * P, scale, 0, sms, st);
   if (e == cudaSuccess) e = mmk::launch_scale_copy(B, Bs, P * M, scale, 1, sms, st);
-  if (e == cudaSuccess) e = mmk::launch_winograd(As, Bs, C, y, z, N, P, M, st);
+  if (e == cudaSuccess) e = mmk::launch_winograd(As, Bs, C, y, z, N, P, M, st, sms);
   if (e == cudaSuccess && lambda_out) {
     e = cudaMemcpyAsync(lambda_out, lam, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

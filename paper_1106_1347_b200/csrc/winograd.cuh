@@ -13,12 +13,14 @@
 // scalings, lambda read from device memory written by lambda_kernel -- no host round trip).
 //
 // Kernels:
-//  * winograd_yz_kernel: y (one thread per row, A staged through shared memory in
-//    coalesced 32 x 32 tiles) and z (one thread per column, coalesced) -- sequential sums.
-//  * winograd_kernel: CTA 64 x 128, 256 threads, 4 x 8 outputs per thread; the pair loop
-//    covers columns 0..2*gamma-1 only (the odd column never enters acc).
+//  * winograd_yz_kernel: y (one lane per row of A) and z (one lane per column of B), 32 x 32
+//    tiles streamed through a cp.async ring -- sequential sums, HBM-bound.
+//  * winograd_kernel: SimtCfg tiles (below); the pair loop covers columns 0..2*gamma-1 only
+//    (the odd column never enters acc).
 #pragma once
 #include "simt_tile.cuh"
+
+#include <type_traits>
 
 namespace mmk {
 
@@ -42,51 +44,78 @@ __global__ void __launch_bounds__(256) scale_copy_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------- y / z prologue
+// One warp owns 32 "lines": 32 rows of A (y) or 32 columns of B (z).  32 x 32 tiles stream
+// through a 4-deep cp.async ring (every global read a coalesced 256-byte row segment) and
+// each lane accumulates its own line in increasing j -- the oracle's order.
 namespace wyz {
-constexpr int THREADS = 128;  // rows (or columns) per block
-constexpr int TILE_K = 32;    // columns of A staged per step (16 pairs)
+constexpr int LINES = 32, TK = 32, STAGES = 4;
 }  // namespace wyz
 
-// blocks [0, nb_y) compute y for rows [128 b, 128 b + 128); blocks [nb_y, ...) compute z.
-__global__ void __launch_bounds__(wyz::THREADS) winograd_yz_kernel(const double* __restrict__ A,
-                                                                   const double* __restrict__ B,
-                                                                   double* __restrict__ y, double* __restrict__ z,
-                                                                   int64_t N, int64_t P, int64_t M, int nb_y) {
+// blocks [0, nb_y) compute y for rows [32 b, 32 b + 32); blocks [nb_y, ...) compute z.
+__global__ void __launch_bounds__(32) winograd_yz_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                         double* __restrict__ y, double* __restrict__ z, int64_t N,
+                                                         int64_t P, int64_t M, int nb_y) {
   using namespace wyz;
-  __shared__ double tileA[THREADS][TILE_K + 1];
-  const int tid = threadIdx.x;
-  const int64_t gamma = P / 2;
-  if (int(blockIdx.x) < nb_y) {
-    const int64_t r0 = int64_t(blockIdx.x) * THREADS;
-    const int64_t kend = 2 * gamma;
-    double acc = 0.0;
-    for (int64_t k0 = 0; k0 < kend; k0 += TILE_K) {
-      // coalesced stage of rows r0..r0+127, columns k0..k0+31: each warp reads 32 consecutive doubles of a row
-      __syncthreads();
-      for (int e = tid; e < THREADS * TILE_K; e += THREADS) {
-        const int rr = e / TILE_K, kk = e % TILE_K;
-        const int64_t gr = r0 + rr, gk = k0 + kk;
-        tileA[rr][kk] = (gr < N && gk < kend) ? A[gr * P + gk] : 0.0;
-      }
-      __syncthreads();
-      const int64_t rem_k = kend - k0;
-      const int npairs = int(rem_k < TILE_K ? rem_k : TILE_K) / 2;
-      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tileA[tid][2 * j], tileA[tid][2 * j + 1]));
-    }
-    const int64_t row = r0 + tid;
-    if (row < N) y[row] = acc;
-  } else {
-    const int64_t col = int64_t(blockIdx.x - nb_y) * THREADS + tid;
-    if (col >= M) return;
-    double acc = 0.0;
+  __shared__ __align__(16) double tile[STAGES][LINES][TK + 1];
+  const int lane = threadIdx.x;
+  const bool is_y = int(blockIdx.x) < nb_y;
+  const int64_t l0 = int64_t(is_y ? blockIdx.x : blockIdx.x - nb_y) * LINES;
+  const int64_t kend = 2 * (P / 2);  // the odd column / row never enters y or z
+  const int64_t KT = cdiv(kend, TK);
+  // y: tile[s][r][c] = A[l0 + r][k0 + c];  z: tile[s][r][c] = B[k0 + r][l0 + c]
+  auto load = [&](int64_t kt, int s) {
+    const int64_t k0 = kt * TK;
 #pragma unroll 8
-    for (int64_t j = 0; j < gamma; ++j) acc = dadd(acc, dmul(B[(2 * j) * M + col], B[(2 * j + 1) * M + col]));
-    z[col] = acc;
+    for (int r = 0; r < LINES; ++r) {
+      if (is_y) {
+        const int64_t gr = l0 + r, gk = k0 + lane;
+        const bool v = gr < N && gk < kend;
+        cp_async8(&tile[s][r][lane], v ? A + gr * P + gk : A, v);
+      } else {
+        const int64_t gk = k0 + r, gc = l0 + lane;
+        const bool v = gk < kend && gc < M;
+        cp_async8(&tile[s][r][lane], v ? B + gk * M + gc : B, v);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load(s, s);
+    cp_async_commit();
+  }
+  double acc = 0.0;
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();
+    {
+      const int64_t nk = kt + STAGES - 1;
+      if (nk < KT) load(nk, int(nk % STAGES));
+      cp_async_commit();
+    }
+    const int s = int(kt % STAGES);
+    const int64_t rem = kend - kt * TK;
+    const int npairs = int(rem < TK ? rem : TK) / 2;
+    if (is_y) {
+      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tile[s][lane][2 * j], tile[s][lane][2 * j + 1]));
+    } else {
+      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tile[s][2 * j][lane], tile[s][2 * j + 1][lane]));
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  const int64_t idx = l0 + lane;
+  if (is_y) {
+    if (idx < N) y[idx] = acc;
+  } else {
+    if (idx < M) z[idx] = acc;
   }
 }
 
 // ---------------------------------------------------------------- main pair-sum kernel
-using WinogradDefault = SimtCfg<64, 128, 4, 8, 3, 1>;
+// 128 x 64 tiles, 128 threads of 8 x 8 outputs, 2 CTAs per SM; 64 x 64 tiles of 4 x 8 when the
+// big tiles would leave SMs idle (tools/tune/simt_tune.cu, profiles/r01/simt_tune*.jsonl)
+using WinogradDefault = SimtCfg<128, 64, 8, 8, 3, 2>;
+using WinogradSmall = SimtCfg<64, 64, 4, 8, 3, 2>;
 
 // The tiles are loaded with kend = 2*gamma: columns/rows >= 2*gamma are zero-filled, so the
 // odd column never enters acc.  A zero-filled pair adds (0+0)(0+0) = +0 to acc, which leaves
@@ -204,24 +233,35 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
 
 inline cudaError_t launch_winograd_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P,
                                       int64_t M, cudaStream_t st) {
-  const int nb_y = int(cdiv(N, wyz::THREADS));
-  const int nb_z = int(cdiv(M, wyz::THREADS));
-  winograd_yz_kernel<<<nb_y + nb_z, wyz::THREADS, 0, st>>>(A, B, y, z, N, P, M, nb_y);
+  const int nb_y = int(cdiv(N, wyz::LINES));
+  const int nb_z = int(cdiv(M, wyz::LINES));
+  winograd_yz_kernel<<<nb_y + nb_z, 32, 0, st>>>(A, B, y, z, N, P, M, nb_y);
   note_launch();
   return cudaGetLastError();
 }
 
 // y, z: device buffers of N and M doubles.
-template <class CF = WinogradDefault>
-inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
-                                   int64_t P, int64_t M, cudaStream_t st) {
-  cudaError_t e = launch_winograd_yz(A, B, y, z, N, P, M, st);
-  if (e != cudaSuccess) return e;
+template <class CF>
+inline cudaError_t launch_winograd_main(const double* A, const double* B, double* C, const double* y,
+                                        const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
   if (av && bv && cv) return launch_winograd_t<CF, 2, 2, 2>(A, B, C, y, z, N, P, M, st);
   if (bv && cv) return launch_winograd_t<CF, 1, 2, 2>(A, B, C, y, z, N, P, M, st);
   return launch_winograd_t<CF, 1, 1, 1>(A, B, C, y, z, N, P, M, st);
+}
+
+template <class CF = void>
+inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
+                                   int64_t P, int64_t M, cudaStream_t st, int sms = 148) {
+  cudaError_t e = launch_winograd_yz(A, B, y, z, N, P, M, st);
+  if (e != cudaSuccess) return e;
+  if (!std::is_void<CF>::value)
+    return launch_winograd_main<typename std::conditional<std::is_void<CF>::value, WinogradDefault, CF>::type>(
+        A, B, C, y, z, N, P, M, st);
+  const int64_t big_tiles = cdiv(N, WinogradDefault::BM) * cdiv(M, WinogradDefault::BN);
+  if (big_tiles >= 2 * int64_t(sms)) return launch_winograd_main<WinogradDefault>(A, B, C, y, z, N, P, M, st);
+  return launch_winograd_main<WinogradSmall>(A, B, C, y, z, N, P, M, st);
 }
 
 inline cudaError_t launch_scale_copy(const double* src, double* dst, int64_t n, const double* scale, int which,

@@ -1,0 +1,111 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the row-block driver paper_1106_1347_b200.dist:
+sharding, the B broadcast, the max-all-reduce of ||A||_inf and the resulting lambda.  The local
+compute is injected (the oracle), so this exercises exactly the host-side logic the GPU path
+uses, and checks the per-rank results are bitwise the rows of the 1-process product."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_compute(method, A, B, out, levels, norms):
+    import oracle
+
+    A_np, B_np = A.numpy(), B.numpy()
+    if method == "naive":
+        C = oracle.naive_fma(A_np, B_np)
+    elif method == "kahan":
+        C = oracle.naive_kahan(A_np, B_np)
+    elif method == "winograd":
+        C = oracle.winograd_original(A_np, B_np)
+    elif method == "winograd_scaled":
+        lam = oracle.lam(float(norms[0]), float(norms[1]))
+        idx = [(i, j) for i in range(A_np.shape[0]) for j in range(B_np.shape[1])]
+        C = oracle.entries(oracle.M_WINOGRAD_SCALED, A_np, B_np, idx, lam).reshape(A_np.shape[0], B_np.shape[1])
+    else:
+        raise ValueError(method)
+    return torch.from_numpy(C)
+
+
+def _oracle_norm(X):
+    import oracle
+
+    return torch.tensor([oracle.norm_inf(X.numpy())], dtype=torch.float64)
+
+
+def _worker(rank, world, port, N, P, M, seed, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workload
+        from paper_1106_1347_b200.dist import dist_gemm, shard_rows
+
+        A, B = workload.custom(N, P, M, seed=seed)
+        A = A * 1e5  # make lambda non-zero
+        lo, hi = shard_rows(N, world, rank)
+        assert (lo, hi) == workload.shard_rows(N, world, rank)
+        A_loc = torch.from_numpy(np.ascontiguousarray(A[lo:hi]))
+        Bt = torch.from_numpy(B.copy()) if rank == 0 else torch.zeros((P, M), dtype=torch.float64)
+        out = {}
+        for m in ("naive", "kahan", "winograd", "winograd_scaled"):
+            C = dist_gemm(m, A_loc, Bt, compute=_oracle_compute, norm=_oracle_norm)
+            out[m] = C.numpy().copy()
+        assert np.array_equal(Bt.numpy(), B)  # broadcast delivered B everywhere
+        q.put((rank, lo, hi, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, N, P, M, seed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, P, M, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res, key=lambda r: r[0])
+
+
+@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16)])
+def test_row_sharded_bitwise(shape):
+    import oracle
+    import workload
+
+    N, P, M = shape
+    res = _run(2, N, P, M, seed=N + P + M)
+    A, B = workload.custom(N, P, M, seed=N + P + M)
+    A = A * 1e5
+    full = {
+        "naive": oracle.naive_fma(A, B),
+        "kahan": oracle.naive_kahan(A, B),
+        "winograd": oracle.winograd_original(A, B),
+        "winograd_scaled": oracle.winograd_scaled(A, B)[0],
+    }
+    assert oracle.winograd_scaled(A, B)[1] != 0
+    for rank, lo, hi, out in res:
+        for m, C in out.items():
+            assert C.shape == (hi - lo, M)
+            assert np.array_equal(C, full[m][lo:hi]), (rank, m)
+    assert sum(hi - lo for _, lo, hi, _ in res) == N

@@ -91,19 +91,17 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB>
-  wino<SimtCfg<64, 128, 4, 8, 3, 1>>("64x128_t4x8_s3", c, true);
-  wino<SimtCfg<64, 64, 4, 4, 3, 2>>("64x64_t4x4_s3_2cta", c, false);
-  wino<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, false);
-  wino<SimtCfg<32, 128, 4, 8, 3, 2>>("32x128_t4x8_s3_2cta", c, false);
-  wino<SimtCfg<64, 128, 4, 4, 3, 1>>("64x128_t4x4_s3", c, false);
-  wino<SimtCfg<128, 128, 8, 8, 3, 1>>("128x128_t8x8_s3", c, false);
-  wino<SimtCfg<128, 64, 8, 4, 3, 2>>("128x64_t8x4_s3_2cta", c, false);
-  wino<SimtCfg<64, 64, 4, 4, 2, 3>>("64x64_t4x4_s2_3cta", c, false);
-  kahan<SimtCfg<64, 128, 4, 8, 3, 1>>("64x128_t4x8_s3", c, true);
-  kahan<SimtCfg<64, 64, 4, 4, 3, 2>>("64x64_t4x4_s3_2cta", c, false);
-  kahan<SimtCfg<32, 128, 4, 8, 3, 2>>("32x128_t4x8_s3_2cta", c, false);
-  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, false);
-  kahan<SimtCfg<64, 128, 4, 4, 3, 1>>("64x128_t4x4_s3", c, false);
-  kahan<SimtCfg<64, 64, 4, 4, 2, 3>>("64x64_t4x4_s2_3cta", c, false);
+  wino<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, true);
+  wino<SimtCfg<64, 64, 4, 8, 4, 2>>("64x64_t4x8_s4_2cta", c, false);
+  wino<SimtCfg<64, 128, 8, 8, 3, 2>>("64x128_t8x8_s3_2cta", c, false);
+  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("128x64_t8x8_s3_2cta", c, false);
+  wino<SimtCfg<64, 64, 8, 4, 3, 2>>("64x64_t8x4_s3_2cta", c, false);
+  wino<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
+  wino<SimtCfg<64, 64, 8, 8, 3, 4>>("64x64_t8x8_s3_4cta", c, false);
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, true);
+  kahan<SimtCfg<64, 64, 4, 8, 4, 2>>("64x64_t4x8_s4_2cta", c, false);
+  kahan<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
+  kahan<SimtCfg<64, 32, 4, 8, 3, 3>>("64x32_t4x8_s3_3cta", c, false);
+  kahan<SimtCfg<64, 64, 8, 4, 3, 2>>("64x64_t8x4_s3_2cta", c, false);
   return 0;
 }
