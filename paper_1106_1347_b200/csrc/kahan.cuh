@@ -24,7 +24,7 @@ __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double
                                            const double* As, const double* Bs, int kk, int ty, int tx) {
   double a[CF::TM], b[CF::TN];
 #pragma unroll
-  for (int i = 0; i < CF::TM; ++i) a[i] = As[(CF::TM * ty + i) * CF::APITCH + kk];
+  for (int i = 0; i < CF::TM; ++i) a[i] = As[simt_row<CF>(ty, i) * CF::APITCH + kk];
 #pragma unroll
   for (int c = 0; c < CF::TN / 2; ++c) {
     double2 v = *reinterpret_cast<const double2*>(Bs + kk * CF::BN + 2 * tx + 2 * CF::TXN * c);
@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   double* As_base = smem;
   double* Bs_base = smem + STAGES * CF::A_ELEMS;
   const int tid = threadIdx.x, tx = tid % CF::TXN, ty = tid / CF::TXN;
-  const int64_t m0 = int64_t(blockIdx.y) * CF::BM, n0 = int64_t(blockIdx.x) * CF::BN;
+  int64_t m0, n0;
+  simt_tile_coords(N, M, CF::BM, CF::BN, m0, n0);
 
   double sum[CF::TM][CF::TN], err[CF::TM][CF::TN];
 #pragma unroll
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 
 #pragma unroll
   for (int i = 0; i < CF::TM; ++i) {
-    const int64_t row = m0 + CF::TM * ty + i;
+    const int64_t row = m0 + simt_row<CF>(ty, i);
     if (row >= N) continue;
 #pragma unroll
     for (int c = 0; c < CF::TN / 2; ++c) {
@@ -119,7 +120,7 @@ cudaError_t launch_kahan_t(const double* A, const double* B, double* C, int64_t 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(unsigned(cdiv(M, CF::BN)), unsigned(cdiv(N, CF::BM)));
+  dim3 grid(unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM)));
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(A, B, C, N, P, M);
   note_launch();
   return cudaGetLastError();

@@ -63,4 +63,25 @@ __device__ __forceinline__ void simt_load_tile(double* As, double* Bs, const dou
   }
 }
 
+// Output row of thread row-index ty, i-th of its TM rows: rows are interleaved across threads
+// (ty + TYM*i) so that the A-row reads of the different ty in one warp fall in different
+// bank groups (APITCH = 18 doubles, TYM*... consecutive rows are 144 B apart).
+template <class CF>
+__device__ __forceinline__ int simt_row(int ty, int i) {
+  return ty + CF::TYM * i;
+}
+
+// Grouped rasterisation of a 1-D grid of BM x BN tiles (8 tile rows per group) for L2 reuse.
+__device__ __forceinline__ void simt_tile_coords(int64_t N, int64_t M, int BM, int BN, int64_t& m0, int64_t& n0) {
+  constexpr int GROUP = 8;
+  const int64_t tiles_m = cdiv(N, BM), tiles_n = cdiv(M, BN);
+  const int64_t tile = blockIdx.x;
+  const int64_t group = tile / (GROUP * tiles_n);
+  const int64_t first = group * GROUP;
+  const int64_t gsize = (tiles_m - first) < GROUP ? (tiles_m - first) : GROUP;
+  const int64_t in_group = tile - group * GROUP * tiles_n;
+  m0 = (first + in_group % gsize) * BM;
+  n0 = (in_group / gsize) * BN;
+}
+
 }  // namespace mmk

@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   double* As_base = smem;
   double* Bs_base = smem + STAGES * CF::A_ELEMS;
   const int tid = threadIdx.x, tx = tid % CF::TXN, ty = tid / CF::TXN;
-  const int64_t m0 = int64_t(blockIdx.y) * CF::BM, n0 = int64_t(blockIdx.x) * CF::BN;
+  int64_t m0, n0;
+  simt_tile_coords(N, M, CF::BM, CF::BN, m0, n0);
   const int64_t Kend = 2 * (P / 2);
 
   double acc[TM][TN];
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
       double a0[TM], a1[TM], b0[TN], b1[TN];
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        double2 v = *reinterpret_cast<const double2*>(As + (TM * ty + i) * CF::APITCH + 2 * jp);
+        double2 v = *reinterpret_cast<const double2*>(As + simt_row<CF>(ty, i) * CF::APITCH + 2 * jp);
         a0[i] = v.x;
         a1[i] = v.y;
       }
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   const bool odd = (P & 1) != 0;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int64_t row = m0 + TM * ty + i;
+    const int64_t row = m0 + simt_row<CF>(ty, i);
     if (row >= N) continue;
     const double yi = y[row];
     const double alast = odd ? A[row * P + (P - 1)] : 0.0;
@@ -225,7 +226,7 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(unsigned(cdiv(M, CF::BN)), unsigned(cdiv(N, CF::BM)));
+  dim3 grid(unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM)));
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(A, B, C, y, z, N, P, M);
   note_launch();
   return cudaGetLastError();
