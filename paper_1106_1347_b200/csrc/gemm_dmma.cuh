@@ -31,9 +31,9 @@ struct GemmProblem {
   int64_t batch;
 };
 
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1, int BK_ = 16>
 struct GemmCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = 16;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_, MIN_BLOCKS = MIN_BLOCKS_;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -44,6 +44,7 @@ struct GemmCfg {
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
   static_assert((A_ELEMS / 2) % THREADS == 0 && (B_ELEMS / 2) % THREADS == 0, "loader split");
   static_assert(BN % 16 == 0, "B swizzle needs BN % 16 == 0");
+  static_assert(BK == 16 || BK == 32, "A swizzle assumes 16- or 32-double rows");
 };
 
 // the production configuration: 128 x 64 tiles, 4 warps of 64 x 32, 4 stages, 2 CTAs per SM
@@ -60,7 +61,7 @@ __device__ __forceinline__ void gemm_load_tile(double* As, double* Bs, const dou
 #pragma unroll
     for (int i = 0; i < (CF::A_ELEMS / 2) / T; ++i) {
       int c = tid + i * T;
-      int r = c >> 3, kp = (c & 7) * 2;
+      int r = c / (BK / 2), kp = (c % (BK / 2)) * 2;
       int64_t gm = m0 + r, gk = k0 + kp;
       bool v = (gm < N) && (gk < P);
       cp_async16(As + r * BK + (kp ^ ((r & 3) << 2)), v ? (A + gm * lda + gk) : A, v);
@@ -69,7 +70,7 @@ __device__ __forceinline__ void gemm_load_tile(double* As, double* Bs, const dou
 #pragma unroll
     for (int i = 0; i < CF::A_ELEMS / T; ++i) {
       int e = tid + i * T;
-      int r = e >> 4, kk = e & 15;
+      int r = e / BK, kk = e % BK;
       int64_t gm = m0 + r, gk = k0 + kk;
       bool v = (gm < N) && (gk < P);
       cp_async8(As + r * BK + (kk ^ ((r & 3) << 2)), v ? (A + gm * lda + gk) : A, v);

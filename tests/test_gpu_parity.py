@@ -269,3 +269,61 @@ def test_host_matmul_e2e():
         assert not C.is_cuda
         assert norm_rows_err(C.numpy(), oracle.naive_standard(A, B)) <= tol_for(name) * oracle.norm_inf(
             A) * oracle.norm_inf(B)
+
+
+# ------------------------------------------------------------------ config c4 (8192^3, bench.py's workload; sampled)
+@pytest.fixture(scope="module")
+def c4_ops():
+    A, B = workload.operands("c4")
+    return A, B, dev(A), dev(B)
+
+
+@pytest.mark.parametrize("method,levels", [("naive", 0), ("kahan", 0), ("winograd", 0), ("winograd_scaled", 0),
+                                           ("strassen", 2), ("strassen_winograd", 2), ("strassen_winograd", 3)])
+def test_c4_sampled(method, levels, c4_ops):
+    """BASELINE.json config 4 at full size, in bench.py's launch configuration: 4096 seeded
+    entries + 2 full rows against the oracle's per-entry replicas (bitwise), and the inf-norm
+    bar on the full rows against the literal NaivStandard."""
+    A, B, dA, dB = c4_ops
+    N, P, M = A.shape[0], A.shape[1], B.shape[1]
+    C = host(run(method, dA, dB, levels))
+    idx = _sample(4, N, M, 4096)
+    rows = [int(r) for r in workload.sample_positions(4, N, 1, 2, 9)[:, 0]]
+    idx_rows = [(r, j) for r in rows for j in range(M)]
+    allidx = idx + idx_rows
+    if method.startswith("strassen"):
+        d, pad = plan_pad(N, P, M, levels)
+        ref = oracle.entries_strassen(0 if method == "strassen" else 1, A, B, allidx, levels=d, pad=pad,
+                                      base=oracle.BASE_FMA)
+    else:
+        lam = oracle.lam(oracle.norm_inf(A), oracle.norm_inf(B))
+        m = {"naive": oracle.M_FMA, "kahan": oracle.M_KAHAN, "winograd": oracle.M_WINOGRAD,
+             "winograd_scaled": oracle.M_WINOGRAD_SCALED}[method]
+        ref = oracle.entries(m, A, B, allidx, lam)
+    got = np.array([C[i, j] for i, j in allidx])
+    assert np.array_equal(got, ref), (method, np.abs(got - ref).max())
+    lit = oracle.entries(oracle.M_STANDARD, A, B, idx_rows).reshape(len(rows), M)
+    assert norm_rows_err(C[rows], lit) <= tol_for(method) * oracle.norm_inf(A) * oracle.norm_inf(B)
+
+
+# ------------------------------------------------------------------ config c5: one rank's shard of the 8-GPU run
+def test_c5_rank_shard_sampled():
+    """BASELINE.json config 5 (32768^3) as one rank of the 8-GPU row-block run sees it:
+    rows [0, 4096) of A times the full B.  2048 seeded entries per method, bitwise against
+    the oracle (classical and Strassen-Winograd, the two methods config 5 names)."""
+    cfg = workload.CONFIGS["c5"]
+    lo, hi = workload.shard_rows(cfg.N, 8, 0)
+    A = workload.matrix(cfg, 0, 0, lo, hi)
+    B = workload.matrix(cfg, 1, 0)
+    dA, dB = dev(A), dev(B)
+    N, P, M = A.shape[0], A.shape[1], B.shape[1]
+    idx = _sample(5, N, M, 2048, shard=0)
+    C = host(mm.naive(dA, dB))
+    ref = oracle.entries(oracle.M_FMA, A, B, idx)
+    assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
+    del C
+    C = host(mm.strassen_winograd(dA, dB, levels=2))
+    d, pad = plan_pad(N, P, M, 2)
+    ref = oracle.entries_strassen(1, A, B, idx, levels=d, pad=pad, base=oracle.BASE_FMA)
+    assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
+    mm.release_workspace()

@@ -1,0 +1,68 @@
+"""Per-config, per-method device timings on one B200.
+
+For each BASELINE.json config that fits one GPU (c1-c4) and each method: median of R timed
+calls (CUDA events, inputs resident), GFLOP/s as 2NPM/t, fraction of the 37.22 TF FP64
+peak, and the error against NaivKahan on the device as ||C - N||_inf / (||A|| ||B||)
+(the paper's stability column).  Writes JSON lines to stdout.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_1106_1347_b200 as mm
+import workload
+
+PEAK = 37.22
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    methods = [("naive", None), ("kahan", None), ("winograd", None), ("winograd_scaled", None),
+               ("strassen", 1), ("strassen", 2), ("strassen", 3), ("strassen_winograd", 1),
+               ("strassen_winograd", 2), ("strassen_winograd", 3), ("strassen_winograd", -1)]
+    for key in a.configs.split(","):
+        cfg = workload.CONFIGS[key]
+        A_h, B_h = workload.operands(key)
+        A = torch.from_numpy(A_h).cuda()
+        B = torch.from_numpy(B_h).cuda()
+        del A_h, B_h
+        nA, nB = mm.norm_inf(A).item(), mm.norm_inf(B).item()
+        K = mm.kahan(A, B)
+        C = torch.empty_like(K)
+        for name, lv in methods:
+            if lv == -1 and cfg.N > 2048:
+                continue  # the paper's plan recurses to order-17 bases: only for small sizes
+            f = getattr(mm, name)
+            kw = {"levels": lv} if lv is not None else {}
+            f(A, B, out=C, **kw)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                f(A, B, out=C, **kw)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = statistics.median(ts)
+            err = (C - K).abs().sum(dim=1).max().item() / (nA * nB) if name != "kahan" else 0.0
+            g = 2.0 * cfg.N * cfg.P * cfg.M / ms / 1e6
+            print(json.dumps({"config": key, "N": cfg.N, "P": cfg.P, "M": cfg.M, "method": name, "levels": lv,
+                              "ms": round(ms, 4), "gflops": round(g, 1), "frac_fp64_peak": round(g / 1e3 / PEAK, 4),
+                              "rel_err_vs_kahan": err}), flush=True)
+        mm.release_workspace()
+        del A, B, C, K
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -70,14 +70,10 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
   run<GemmCfg<128, 64, 2, 2, 4, 2>>("128x64_w2x2_s4_2cta", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<128, 64, 2, 2, 3, 2>>("128x64_w2x2_s3_2cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 128, 1, 4, 4, 2>>("64x128_w1x4_s4_2cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 128, 1, 4, 3, 2>>("64x128_w1x4_s3_2cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 128, 2, 2, 4, 2>>("64x128_w2x2_s4_2cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 1, 2, 3, 4>>("64x64_w1x2_s3_4cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 1, 2, 2, 4>>("64x64_w1x2_s2_4cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<128, 32, 2, 1, 4, 3>>("128x32_w2x1_s4_3cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 4>>("64x64_w2x2_s4_4cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 3, 5>>("64x64_w2x2_s3_5cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 2, 2, 2, 2, 32>>("128x64_w2x2_s2_2cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 2, 2, 3, 1, 32>>("128x64_w2x2_s3_1cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 3, 3, 32>>("64x64_w2x2_s3_3cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 128, 2, 4, 3, 1, 32>>("128x128_w2x4_s3_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 128, 1, 4, 2, 2, 32>>("64x128_w1x4_s2_2cta_bk32", A, B, C, R, n, reps, bad);
   return 0;
 }
