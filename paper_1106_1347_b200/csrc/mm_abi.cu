@@ -101,9 +101,10 @@ int32_t mm_lambda(double nA, double nB) { return mmk::lambda_rule(nA, nB); }
 int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
-  if ((rc = check_device(nullptr))) return rc;
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
   mmk::GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
-  return cuda_status(mmk::launch_dgemm(pr, S(stream)));
+  return cuda_status(mmk::launch_dgemm(pr, S(stream), sms));
 }
 
 int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {

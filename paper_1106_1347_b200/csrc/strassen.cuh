@@ -312,7 +312,7 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   const int d = pl.depth;
   if (d == 0) {
     GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
-    return launch_dgemm(pr, st);
+    return launch_dgemm(pr, st, sms);
   }
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   cudaError_t e;
@@ -353,7 +353,7 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   {
     const int64_t n = pl.Np >> d, p = pl.Pp >> d, m = pl.Mp >> d;
     GemmProblem pr{S[0], T[0], Hb, n, p, m, p, m, m, n * p, p * m, n * m, ipow7(d)};
-    e = launch_dgemm(pr, st);
+    e = launch_dgemm(pr, st, sms);
     if (e != cudaSuccess) return e;
   }
   for (int l = d - 1; l >= 0; --l) {

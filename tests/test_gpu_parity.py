@@ -327,3 +327,18 @@ def test_c5_rank_shard_sampled():
     ref = oracle.entries_strassen(1, A, B, idx, levels=d, pad=pad, base=oracle.BASE_FMA)
     assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
     mm.release_workspace()
+
+
+def test_host_matmul_pipelined_bitwise():
+    """matmul() on pinned host tensors pipelines A/C by row blocks for the row-local methods;
+    the result must be bitwise the oracle's (and the one-shot device call's)."""
+    A, B = workload.custom(515, 130, 257, seed=11)
+    hA = torch.from_numpy(A).pin_memory()
+    hB = torch.from_numpy(B).pin_memory()
+    refs = {"naive": oracle.naive_fma(A, B), "kahan": oracle.naive_kahan(A, B),
+            "winograd": oracle.winograd_original(A, B)}
+    for name, ref in refs.items():
+        for rb in (1, 3, 4):
+            out = torch.empty((515, 257), dtype=torch.float64).pin_memory()
+            C = mm.matmul(hA, hB, name, out=out, row_blocks=rb)
+            assert np.array_equal(C.numpy(), ref), (name, rb)

@@ -30,7 +30,7 @@ void run(const char* name, const double* A, const double* B, double* C, const do
          unsigned long long* bad) {
   GemmProblem pr{A, B, C, n, n, n, n, n, n, 0, 0, 0, 1};
   cudaMemset(C, 0, n * n * 8);
-  if (launch_dgemm<CF>(pr, 0) != cudaSuccess) {
+  if (launch_dgemm_cfg<CF>(pr, 0) != cudaSuccess) {
     printf("{\"cfg\":\"%s\",\"error\":\"%s\"}\n", name, cudaGetErrorString(cudaGetLastError()));
     return;
   }
@@ -39,7 +39,7 @@ void run(const char* name, const double* A, const double* B, double* C, const do
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) launch_dgemm<CF>(pr, 0);
+  for (int r = 0; r < reps; ++r) launch_dgemm_cfg<CF>(pr, 0);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
