@@ -15,48 +15,65 @@
 
 namespace mmk {
 
-namespace nrm {
-constexpr int ROWS = 32;  // rows per block (one warp)
-constexpr int TK = 32;    // columns per stage
-constexpr int STAGES = 4;
-}  // namespace nrm
+// ---- line streaming: one warp owns 32 "lines" (rows of X, or columns of X) and streams them
+// through shared memory in 32 x LS_TK tiles with an LS_STAGES-deep cp.async ring; every global
+// read is a coalesced 256-byte segment and each lane then walks its own line in index order.
+constexpr int LS_LINES = 32, LS_TK = 64, LS_STAGES = 5;
+constexpr int LS_ROWPITCH = LS_TK + 1;       // row-lines tile [32][TK+1]  (lane reads its row)
+constexpr int LS_COLPITCH = LS_LINES + 1;    // column-lines tile [TK][33] (lane reads its column)
+constexpr int LS_TILE = LS_LINES * LS_ROWPITCH > LS_TK * LS_COLPITCH ? LS_LINES * LS_ROWPITCH : LS_TK * LS_COLPITCH;
+constexpr size_t LS_SMEM = size_t(LS_STAGES) * LS_TILE * sizeof(double);
 
-__global__ void __launch_bounds__(nrm::ROWS) norm_inf_kernel(const double* __restrict__ X, int64_t rows,
-                                                             int64_t cols, unsigned long long* __restrict__ out) {
-  using namespace nrm;
-  __shared__ __align__(16) double tile[STAGES][ROWS][TK + 1];
-  const int lane = threadIdx.x;
-  const int64_t r0 = int64_t(blockIdx.x) * ROWS;
-  const int64_t KT = cdiv(cols, TK);
-  auto load = [&](int64_t kt, int s) {
-    const int64_t c0 = kt * TK;
-    // each lane copies column c0+lane of all 32 rows: one 256-byte coalesced row segment per step
+// rows [r0, r0+32) x columns [c0, c0+TK) of row-major X (ld) -> t[r][c]; zero outside rv x cv
+__device__ __forceinline__ void ls_load_rowlines(double* t, const double* __restrict__ X, int64_t ld, int64_t r0,
+                                                 int64_t c0, int64_t rv, int64_t cv, int lane) {
 #pragma unroll 8
-    for (int rr = 0; rr < ROWS; ++rr) {
-      const int64_t gr = r0 + rr, gc = c0 + lane;
-      const bool v = gr < rows && gc < cols;
-      cp_async8(&tile[s][rr][lane], v ? X + gr * cols + gc : X, v);
-    }
-  };
+  for (int r = 0; r < LS_LINES; ++r) {
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load(s, s);
+    for (int h = 0; h < LS_TK / 32; ++h) {
+      const int64_t gr = r0 + r, gc = c0 + lane + 32 * h;
+      const bool v = gr < rv && gc < cv;
+      cp_async8(t + r * LS_ROWPITCH + lane + 32 * h, v ? X + gr * ld + gc : X, v);
+    }
+  }
+}
+
+// rows [k0, k0+TK) x columns [l0, l0+32) of row-major X (ld) -> t[k][c]; zero outside kv x lv
+__device__ __forceinline__ void ls_load_collines(double* t, const double* __restrict__ X, int64_t ld, int64_t k0,
+                                                 int64_t l0, int64_t kv, int64_t lv, int lane) {
+#pragma unroll 8
+  for (int k = 0; k < LS_TK; ++k) {
+    const int64_t gk = k0 + k, gc = l0 + lane;
+    const bool v = gk < kv && gc < lv;
+    cp_async8(t + k * LS_COLPITCH + lane, v ? X + gk * ld + gc : X, v);
+  }
+}
+
+__global__ void __launch_bounds__(LS_LINES) norm_inf_kernel(const double* __restrict__ X, int64_t rows,
+                                                            int64_t cols, unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) double ls_smem[];
+  const int lane = threadIdx.x;
+  const int64_t r0 = int64_t(blockIdx.x) * LS_LINES;
+  const int64_t KT = cdiv(cols, LS_TK);
+#pragma unroll
+  for (int s = 0; s < LS_STAGES - 1; ++s) {
+    if (s < KT) ls_load_rowlines(ls_smem + s * LS_TILE, X, cols, r0, int64_t(s) * LS_TK, rows, cols, lane);
     cp_async_commit();
   }
   double sum = 0.0;
   for (int64_t kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<LS_STAGES - 2>();
     __syncwarp();
     {
-      const int64_t nk = kt + STAGES - 1;
-      if (nk < KT) load(nk, int(nk % STAGES));
+      const int64_t nk = kt + LS_STAGES - 1;
+      if (nk < KT)
+        ls_load_rowlines(ls_smem + (nk % LS_STAGES) * LS_TILE, X, cols, r0, nk * LS_TK, rows, cols, lane);
       cp_async_commit();
     }
-    const int s = int(kt % STAGES);
-    const int64_t rem_c = cols - kt * TK;
-    const int n = int(rem_c < TK ? rem_c : TK);
-    // zero-filled columns would add +0, which is harmless, but stop at the true end anyway
-    for (int j = 0; j < n; ++j) sum = dadd(sum, fabs(tile[s][lane][j]));
+    const double* t = ls_smem + (kt % LS_STAGES) * LS_TILE + lane * LS_ROWPITCH;
+    const int64_t rem_c = cols - kt * LS_TK;
+    const int n = int(rem_c < LS_TK ? rem_c : LS_TK);
+    for (int j = 0; j < n; ++j) sum = dadd(sum, fabs(t[j]));  // row sum, left to right
     __syncwarp();
   }
   cp_async_wait<0>();
@@ -99,7 +116,13 @@ inline cudaError_t launch_norm_inf(const double* X, int64_t rows, int64_t cols, 
                                    cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  norm_inf_kernel<<<unsigned(cdiv(rows, nrm::ROWS)), nrm::ROWS, 0, st>>>(X, rows, cols, out);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(norm_inf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS_SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  norm_inf_kernel<<<unsigned(cdiv(rows, LS_LINES)), LS_LINES, LS_SMEM, st>>>(X, rows, cols, out);
   note_launch();
   return cudaGetLastError();
 }

@@ -18,6 +18,7 @@
 //  * winograd_kernel: SimtCfg tiles (below); the pair loop covers columns 0..2*gamma-1 only
 //    (the odd column never enters acc).
 #pragma once
+#include "norm_lambda.cuh"
 #include "simt_tile.cuh"
 
 #include <type_traits>
@@ -44,61 +45,48 @@ __global__ void __launch_bounds__(256) scale_copy_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------- y / z prologue
-// One warp owns 32 "lines": 32 rows of A (y) or 32 columns of B (z).  32 x 32 tiles stream
-// through a 4-deep cp.async ring (every global read a coalesced 256-byte row segment) and
-// each lane accumulates its own line in increasing j -- the oracle's order.
-namespace wyz {
-constexpr int LINES = 32, TK = 32, STAGES = 4;
-}  // namespace wyz
-
+// One warp owns 32 lines: 32 rows of A (y) or 32 columns of B (z), streamed through the
+// cp.async line ring of norm_lambda.cuh; each lane accumulates its own line in increasing j
+// (the oracle's order).  HBM-bound: 8 (NP + PM) bytes read.
 // blocks [0, nb_y) compute y for rows [32 b, 32 b + 32); blocks [nb_y, ...) compute z.
-__global__ void __launch_bounds__(32) winograd_yz_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                                                         double* __restrict__ y, double* __restrict__ z, int64_t N,
-                                                         int64_t P, int64_t M, int nb_y) {
-  using namespace wyz;
-  __shared__ __align__(16) double tile[STAGES][LINES][TK + 1];
+__global__ void __launch_bounds__(LS_LINES) winograd_yz_kernel(const double* __restrict__ A,
+                                                               const double* __restrict__ B, double* __restrict__ y,
+                                                               double* __restrict__ z, int64_t N, int64_t P,
+                                                               int64_t M, int nb_y) {
+  extern __shared__ __align__(16) double ls_smem[];
   const int lane = threadIdx.x;
   const bool is_y = int(blockIdx.x) < nb_y;
-  const int64_t l0 = int64_t(is_y ? blockIdx.x : blockIdx.x - nb_y) * LINES;
+  const int64_t l0 = int64_t(is_y ? blockIdx.x : blockIdx.x - nb_y) * LS_LINES;
   const int64_t kend = 2 * (P / 2);  // the odd column / row never enters y or z
-  const int64_t KT = cdiv(kend, TK);
-  // y: tile[s][r][c] = A[l0 + r][k0 + c];  z: tile[s][r][c] = B[k0 + r][l0 + c]
+  const int64_t KT = cdiv(kend, LS_TK);
   auto load = [&](int64_t kt, int s) {
-    const int64_t k0 = kt * TK;
-#pragma unroll 8
-    for (int r = 0; r < LINES; ++r) {
-      if (is_y) {
-        const int64_t gr = l0 + r, gk = k0 + lane;
-        const bool v = gr < N && gk < kend;
-        cp_async8(&tile[s][r][lane], v ? A + gr * P + gk : A, v);
-      } else {
-        const int64_t gk = k0 + r, gc = l0 + lane;
-        const bool v = gk < kend && gc < M;
-        cp_async8(&tile[s][r][lane], v ? B + gk * M + gc : B, v);
-      }
-    }
+    double* t = ls_smem + s * LS_TILE;
+    if (is_y) ls_load_rowlines(t, A, P, l0, kt * LS_TK, N, kend, lane);
+    else ls_load_collines(t, B, M, kt * LS_TK, l0, kend, M, lane);
   };
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < LS_STAGES - 1; ++s) {
     if (s < KT) load(s, s);
     cp_async_commit();
   }
   double acc = 0.0;
   for (int64_t kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<LS_STAGES - 2>();
     __syncwarp();
     {
-      const int64_t nk = kt + STAGES - 1;
-      if (nk < KT) load(nk, int(nk % STAGES));
+      const int64_t nk = kt + LS_STAGES - 1;
+      if (nk < KT) load(nk, int(nk % LS_STAGES));
       cp_async_commit();
     }
-    const int s = int(kt % STAGES);
-    const int64_t rem = kend - kt * TK;
-    const int npairs = int(rem < TK ? rem : TK) / 2;
+    const double* t = ls_smem + (kt % LS_STAGES) * LS_TILE;
+    const int64_t rem = kend - kt * LS_TK;
+    const int npairs = int(rem < LS_TK ? rem : LS_TK) / 2;
     if (is_y) {
-      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tile[s][lane][2 * j], tile[s][lane][2 * j + 1]));
+      const double* row = t + lane * LS_ROWPITCH;
+      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(row[2 * j], row[2 * j + 1]));
     } else {
-      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(tile[s][2 * j][lane], tile[s][2 * j + 1][lane]));
+      for (int j = 0; j < npairs; ++j)
+        acc = dadd(acc, dmul(t[(2 * j) * LS_COLPITCH + lane], t[(2 * j + 1) * LS_COLPITCH + lane]));
     }
     __syncwarp();
   }
@@ -234,9 +222,15 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
 
 inline cudaError_t launch_winograd_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P,
                                       int64_t M, cudaStream_t st) {
-  const int nb_y = int(cdiv(N, wyz::LINES));
-  const int nb_z = int(cdiv(M, wyz::LINES));
-  winograd_yz_kernel<<<nb_y + nb_z, 32, 0, st>>>(A, B, y, z, N, P, M, nb_y);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(winograd_yz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS_SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nb_y = int(cdiv(N, LS_LINES));
+  const int nb_z = int(cdiv(M, LS_LINES));
+  winograd_yz_kernel<<<nb_y + nb_z, LS_LINES, LS_SMEM, st>>>(A, B, y, z, N, P, M, nb_y);
   note_launch();
   return cudaGetLastError();
 }

@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu evidence for a round: (1) the launch list of a short bench run, (2) one --set full capture
-# of the dominant kernels on a short dedicated command.  Each ncu command runs only after the
-# identical plain command exited 0 in this same call.
+# of each dominant kernel, (3) DRAM bytes + duration of every HBM-bound kernel.  Each ncu command
+# runs only after the identical plain command exited 0 in this same call.
 set -u
 OUT=gpurun_out/ncu
 mkdir -p $OUT
@@ -9,7 +9,16 @@ BENCH="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
 $BENCH > $OUT/plain_bench.json 2> $OUT/plain_bench.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $BENCH > $OUT/ncu_bench.log 2>&1
 echo "launch list rc=$?"
-QB="python tools/quick_bench.py --methods naive,kahan,winograd,strassen_winograd --reps 1"
-$QB > $OUT/plain_qb.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"dgemm_dmma|kahan_gemm|winograd_kernel|strassen_form|strassen_combine|winograd_yz" -c 8 -o $OUT/full $QB > $OUT/ncu_full.log 2>&1
-echo "full rc=$?"
+for M in naive kahan winograd; do
+  QB="python tools/quick_bench.py --methods $M --reps 1"
+  case $M in naive) K=dgemm_dmma;; kahan) K=kahan_gemm;; winograd) K=winograd_kernel;; esac
+  $QB > $OUT/plain_qb_$M.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o $OUT/full_$M $QB > $OUT/ncu_full_$M.log 2>&1
+  echo "full $M rc=$?"
+done
+QB="python tools/quick_bench.py --methods winograd_scaled,strassen_winograd --reps 1"
+$QB > $OUT/plain_qb_hbm.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
+    --clock-control none -k regex:"strassen_form|strassen_combine|norm_inf|scale_copy|winograd_yz" --csv \
+    --log-file $OUT/hbm_kernels.csv $QB > $OUT/ncu_hbm.log 2>&1
+echo "hbm rc=$?"

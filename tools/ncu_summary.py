@@ -80,12 +80,16 @@ def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "pr
            "| kernel | launches | total ms | mean ms/launch | share |", "|---|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         md.append(f"| {k} | {n} | {t * 1e3:.3f} | {t * 1e3 / n:.3f} | {100 * t / tot:.1f}% |")
-    hdr, units, data = full_raw(os.path.join(src, "full.ncu-rep"))
-    kn = hdr.index("Kernel Name")
-    md += ["", "## `ncu --set full` capture (tools/quick_bench.py, c4 8192^3)", "",
+    reps = [os.path.join(src, f) for f in sorted(os.listdir(src)) if f.endswith(".ncu-rep")]
+    md += ["", "## `ncu --set full` captures (tools/quick_bench.py, c4 8192^3, one launch per kernel)", "",
            "| kernel | " + " | ".join(m[1] for m in METRICS) + " |", "|---" * (len(METRICS) + 1) + "|"]
     traffic = {}
-    for d in data:
+    rows_all = []
+    for rep in reps:
+        hdr, units, data = full_raw(rep)
+        rows_all += [(hdr, units, d) for d in data]
+    for hdr, units, d in rows_all:
+        kn = hdr.index("Kernel Name")
         vals = []
         rec = {}
         for m, short_name in METRICS:
@@ -110,6 +114,23 @@ def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "pr
         fam = family(d[kn])
         if fam not in traffic and rec.get("dram_read") is not None:
             traffic[fam] = int(rec["dram_read"] + (rec.get("dram_write") or 0))
+    hbm = os.path.join(src, "hbm_kernels.csv")
+    if os.path.exists(hbm):
+        rows = launches(hbm)
+        per = collections.defaultdict(dict)
+        for d in rows:
+            key = (d["ID"], short(d["Kernel Name"]), d["Grid Size"])
+            v = float(d["Metric Value"].replace(",", "")) * UNIT_SCALE.get(d["Metric Unit"], 1)
+            per[key][d["Metric Name"]] = v
+        md += ["", "## HBM-bound kernels (winograd_scaled + strassen_winograd d=2 at c4)", "",
+               "| id | kernel | grid | time ms | DRAM read GB | DRAM write GB | achieved GB/s | dram % |", "|---|---|---|---|---|---|---|---|"]
+        for (i, k, grid), m in sorted(per.items(), key=lambda x: int(x[0][0])):
+            t = m.get("gpu__time_duration.sum", 0)
+            rd, wr = m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
+            md.append(f"| {i} | {k} | {grid} | {t * 1e3:.3f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | "
+                      f"{(rd + wr) / t / 1e9 if t else 0:.0f} | {m.get('dram__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} |")
+            fam = family(k)
+            traffic.setdefault(fam, int(rd + wr))
     md += ["", "Time in seconds, bytes in bytes. `traffic` per launch (DRAM read + write) by kernel:", "",
            "```", json.dumps(traffic, indent=1), "```"]
     with open(os.path.join(dst, "ncu_summary.md"), "w") as f:
