@@ -1,0 +1,356 @@
+// lines.cuh -- order-faithful per-line reductions streamed from HBM (product path).
+//
+// Three steps of the hot path are "one sequential sum per line of a matrix":
+//   * NormInf:          s_i = sum_j |X_ij|, left to right; ||X|| = max_i s_i
+//   * Winograd y:         y_i = sum_{j<gamma} A[i][2j] A[i][2j+1]           (rows of A)
+//   * Winograd z:         z_k = sum_{j<gamma} B[2j][k] B[2j+1][k]           (columns of B)
+// and WinogradScaled needs the exact copies 2^lambda A and 2^-lambda B
+// (MultiplyWithScalar) whose y/z are the sums above taken on the copies.
+//
+// The sums must run in index order (reading R1/R17: the oracle's order; on ill-scaled inputs
+// a different order changes y by ~50, SURVEY PR-7), so one lane owns one line and there is no
+// parallelism inside a line.  The kernel is therefore built to keep HBM busy with few warps:
+//   * one warp = 32 lines, one warp per CTA, a LN_STAGES-deep shared-memory ring of
+//     32 x LN_TK tiles;
+//   * operands with a 16-byte aligned base and even pitch arrive by TMA (2-D tensor maps,
+//     one elected lane issues the tile's box copies, completion counted in bytes on an
+//     mbarrier); 8-byte aligned operands (odd pitch, e.g. P = 1001) fall back to 8-byte
+//     cp.async with cp.async.mbarrier.arrive.noinc on the same barrier;
+//   * row-line tiles use the 128-byte TMA swizzle so the lanes' 16-byte reads of their own
+//     rows are bank-conflict free;
+//   * optional fused scaled copy: the scaled tile is written back coalesced from shared
+//     memory, and y/z are accumulated on the scaled values (dmul(s, x) -- the same single
+//     rounding as the oracle's copy), so WinogradScaled needs one pass over A and B after
+//     the norms instead of copy + y/z passes.
+// Up to two jobs (e.g. rows of A and columns of B) share one launch.
+#pragma once
+#include "tma.cuh"
+
+namespace mmk {
+
+constexpr int LN_LINES = 32, LN_TK = 32, LN_STAGES = 6;
+constexpr int LN_TILE = LN_LINES * LN_TK;  // 8 KB per stage
+constexpr unsigned LN_TILE_BYTES = LN_TILE * sizeof(double);
+constexpr size_t LN_SMEM = 1024 + size_t(LN_STAGES) * LN_TILE * sizeof(double) + LN_STAGES * sizeof(uint64_t);
+static_assert(LN_TK == 32 && LN_LINES == 32, "one lane per tile column / line");
+
+enum { LN_ABS = 0, LN_PAIRS = 1 };
+
+struct LineJob {
+  const double* X;               // row-major matrix with leading dimension ld
+  int64_t ld;
+  int64_t nlines;                // rows (by_rows) or columns
+  int64_t len;                   // elements streamed per line (columns, or rows)
+  int64_t pair_end;              // LN_PAIRS: only elements < pair_end enter the sum (2 floor(P/2))
+  double* out;                   // LN_PAIRS: per-line sums
+  unsigned long long* out_max;   // LN_ABS: max over lines, as the bit pattern of a non-negative double
+  double* copy;                  // optional scaled copy (same shape and ld as X)
+  int by_rows;
+  int op;
+  int scale_sel;                 // -1: unscaled; 0: x 2^lambda; 1: x 2^-lambda (lambda from norms)
+  int bulk;                      // 1: tiles arrive by TMA (map[job]); 0: 8-byte cp.async fallback
+  int blocks;                    // 32-line blocks of this job
+};
+
+struct LineLaunch {
+  CUtensorMap map[2];               // TMA maps of the jobs' operands (when bulk)
+  LineJob job[2];
+  int njobs;
+  const unsigned long long* norms;  // {||A||, ||B||} bit patterns (for scale_sel >= 0)
+  int* lam_out;                     // optional: lambda, written by block 0
+  double* scale_out;                // optional: {2^lambda, 2^-lambda}, written by block 0
+};
+
+// The rule of P:206-208 (reading R7): the integer lambda with 1/2 <= 2^(2 lambda) nA/nB <= 2,
+// exact via frexp; when both candidates qualify take the larger |lambda|; a zero norm gives 0.
+__host__ __device__ inline int lambda_rule(double nA, double nB) {
+  if (nA == 0.0 || nB == 0.0) return 0;
+  int eA, eB;
+  const double mA = frexp(nA, &eA);
+  const double mB = frexp(nB, &eB);
+  const int d = eB - eA;
+  if (d % 2 == 0) return d / 2;
+  if (mA < mB) return (d + 1) / 2;
+  if (mA > mB) return (d - 1) / 2;
+  return d > 0 ? (d + 1) / 2 : (d - 1) / 2;
+}
+
+// ---- tile layouts (doubles).  Row-line tile: lines = rows r, elements = columns c, stored as two
+// TMA boxes of [32 rows][16 columns] with the 128-byte swizzle (16-byte chunk q of row r at chunk
+// q ^ (r % 8)), so that lane r reading its own row 16 bytes at a time is conflict free.
+// Column-line tile: [32 rows k][32 columns l] plain, lane l reads t[k][l].
+__device__ __forceinline__ int ln_rowoff(int r, int c) {
+  return (c >> 4) * (LN_LINES * 16) + r * 16 + ((((c & 15) >> 1) ^ (r & 7)) << 1) + (c & 1);
+}
+
+// issue the copies of tile kt of block-lines [l0, l0+32) into stage buffer t (barrier bar)
+__device__ __forceinline__ void ln_issue(const LineLaunch& L, int ji, double* t, uint64_t* bar, int64_t l0,
+                                         int64_t kt, int lane) {
+  const LineJob& jb = L.job[ji];
+  const int64_t k0 = kt * LN_TK;
+  if (jb.bulk) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bar, LN_TILE_BYTES);
+      if (jb.by_rows) {
+        tma_load_2d(t, &L.map[ji], int(k0), int(l0), bar);
+        tma_load_2d(t + LN_LINES * 16, &L.map[ji], int(k0 + 16), int(l0), bar);
+      } else {
+        tma_load_2d(t, &L.map[ji], int(l0), int(k0), bar);
+      }
+    }
+  } else {
+    const int64_t kv = jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK;              // valid elements along the line
+    const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;  // valid lines
+    if (jb.by_rows) {
+#pragma unroll 8
+      for (int r = 0; r < LN_LINES; ++r) {
+        const bool v = r < lv && lane < kv;
+        cp_async8(t + ln_rowoff(r, lane), v ? jb.X + (l0 + r) * jb.ld + k0 + lane : jb.X, v);
+      }
+    } else {
+#pragma unroll 8
+      for (int k = 0; k < LN_TK; ++k) {
+        const bool v = k < kv && lane < lv;
+        cp_async8(t + k * LN_LINES + lane, v ? jb.X + (k0 + k) * jb.ld + l0 + lane : jb.X, v);
+      }
+    }
+    cp_async_mbar_arrive_noinc(bar);
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ LineLaunch L) {
+  extern __shared__ __align__(1024) unsigned char ln_raw[];
+  // 1024-byte aligned stage buffers (the 128-byte swizzle pattern repeats every 1024 bytes)
+  double* ln_smem = reinterpret_cast<double*>(ln_raw + ((1024 - (smem_u32(ln_raw) & 1023)) & 1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ln_smem + LN_STAGES * LN_TILE);
+  const int lane = threadIdx.x;
+  int b = blockIdx.x, ji = 0;
+  if (L.njobs > 1 && b >= L.job[0].blocks) {
+    b -= L.job[0].blocks;
+    ji = 1;
+  }
+  const LineJob& jb = L.job[ji];
+  const int64_t l0 = int64_t(b) * LN_LINES;
+  const int64_t KT = cdiv(jb.len, LN_TK);
+
+  double s = 1.0;
+  if (jb.scale_sel >= 0) {
+    const double nA = __longlong_as_double(static_cast<long long>(L.norms[0]));
+    const double nB = __longlong_as_double(static_cast<long long>(L.norms[1]));
+    const int lam = lambda_rule(nA, nB);
+    s = ldexp(1.0, jb.scale_sel == 0 ? lam : -lam);
+    if (blockIdx.x == 0 && lane == 0) {
+      if (L.lam_out) L.lam_out[0] = lam;
+      if (L.scale_out) {
+        L.scale_out[0] = ldexp(1.0, lam);
+        L.scale_out[1] = ldexp(1.0, -lam);
+      }
+    }
+  }
+
+  if (lane == 0) {
+    if (jb.bulk) tma_prefetch_desc(&L.map[ji]);
+    for (int st = 0; st < LN_STAGES; ++st) mbar_init(bars + st, jb.bulk ? 1 : LN_LINES);
+    fence_mbar_init();
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int st = 0; st < LN_STAGES; ++st)
+    if (st < KT) ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, st, lane);
+
+  const bool scaled = jb.scale_sel >= 0;
+  double acc = 0.0;
+#pragma unroll 1
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    const int st = int(kt % LN_STAGES);
+    mbar_wait(bars + st, unsigned((kt / LN_STAGES) & 1));
+    const double* t = ln_smem + st * LN_TILE;
+    const int64_t k0 = kt * LN_TK;
+    const int kv = int(jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK);
+    if (jb.by_rows) {
+      // lane = row l0 + lane; its 16-byte chunk q (columns 2q, 2q+1) sits in box q/8 at chunk (q%8)^(lane%8)
+      const double* row = t + lane * 16;
+      auto chunk = [&](int q) {
+        return *reinterpret_cast<const double2*>(row + (q >> 3) * (LN_LINES * 16) + (((q & 7) ^ (lane & 7)) << 1));
+      };
+      if (OP == LN_ABS) {
+        if (kv == LN_TK) {
+#pragma unroll
+          for (int q = 0; q < LN_TK / 2; ++q) {
+            const double2 v = chunk(q);
+            acc = dadd(acc, fabs(v.x));  // row sum, left to right
+            acc = dadd(acc, fabs(v.y));
+          }
+        } else {
+          for (int j = 0; j < kv; ++j) acc = dadd(acc, fabs(t[ln_rowoff(lane, j)]));
+        }
+      } else {
+        // pairs (2q, 2q+1) of this tile that lie below pair_end
+        const int64_t pe = jb.pair_end - k0;
+        const int np = int((pe < kv ? pe : kv) / 2);
+        if (np == LN_TK / 2) {
+#pragma unroll
+          for (int q = 0; q < LN_TK / 2; ++q) {
+            double2 v = chunk(q);
+            if (scaled) v = make_double2(dmul(s, v.x), dmul(s, v.y));
+            acc = dadd(acc, dmul(v.x, v.y));  // y_i += A[i][2j] A[i][2j+1]
+          }
+        } else {
+          for (int q = 0; q < np; ++q) {
+            double2 v = chunk(q);
+            if (scaled) v = make_double2(dmul(s, v.x), dmul(s, v.y));
+            acc = dadd(acc, dmul(v.x, v.y));
+          }
+        }
+      }
+      if (jb.copy) {  // coalesced write of the scaled tile: lane = column
+        const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
+        if (lane < kv)
+          for (int r = 0; r < lv; ++r) jb.copy[(l0 + r) * jb.ld + k0 + lane] = dmul(s, t[ln_rowoff(r, lane)]);
+      }
+    } else {
+      // column lines: lane = column l0 + lane, tile row k = element k0 + k of the line
+      if (OP == LN_ABS) {
+        for (int k = 0; k < kv; ++k) acc = dadd(acc, fabs(t[k * LN_LINES + lane]));
+      } else {
+        const int64_t pe = jb.pair_end - k0;
+        const int np = int((pe < kv ? pe : kv) / 2);
+        if (np == LN_TK / 2) {
+#pragma unroll
+          for (int j = 0; j < LN_TK / 2; ++j) {
+            double x0 = t[(2 * j) * LN_LINES + lane], x1 = t[(2 * j + 1) * LN_LINES + lane];
+            if (scaled) {
+              x0 = dmul(s, x0);
+              x1 = dmul(s, x1);
+            }
+            acc = dadd(acc, dmul(x0, x1));  // z_k += B[2j][k] B[2j+1][k]
+          }
+        } else {
+          for (int j = 0; j < np; ++j) {
+            double x0 = t[(2 * j) * LN_LINES + lane], x1 = t[(2 * j + 1) * LN_LINES + lane];
+            if (scaled) {
+              x0 = dmul(s, x0);
+              x1 = dmul(s, x1);
+            }
+            acc = dadd(acc, dmul(x0, x1));
+          }
+        }
+      }
+      if (jb.copy) {  // lane = column; rows of the panel are 256-byte coalesced stores
+        const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
+        if (lane < lv)
+          for (int k = 0; k < kv; ++k) jb.copy[(k0 + k) * jb.ld + l0 + lane] = dmul(s, t[k * LN_LINES + lane]);
+      }
+    }
+    __syncwarp();  // every lane is done with stage st before it is refilled with tile kt + STAGES
+    {
+      const int64_t nk = kt + LN_STAGES;
+      if (nk < KT) {
+        if (jb.bulk) fence_proxy_async_smem();
+        ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, nk, lane);
+      }
+    }
+  }
+
+  const bool valid = l0 + lane < jb.nlines;
+  if (OP == LN_ABS) {
+    double m = valid ? acc : 0.0;  // max is order-free
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) atomicMax(jb.out_max, static_cast<unsigned long long>(__double_as_longlong(m)));
+  } else {
+    if (valid) jb.out[l0 + lane] = acc;
+  }
+}
+
+// fill the derived fields of a job (blocks; TMA map when the operand allows one)
+inline void ln_finish_job(LineJob& j, CUtensorMap* map) {
+  j.blocks = int(cdiv(j.nlines, LN_LINES));
+  j.bulk = 0;
+  if (tma_ok(j.X, j.ld)) {
+    const int64_t rows = j.by_rows ? j.nlines : j.len, cols = j.by_rows ? j.len : j.nlines;
+    if (j.by_rows)
+      j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_LINES, 16, true);
+    else
+      j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_TK, LN_LINES, false);
+  }
+}
+
+template <int OP>
+inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(line_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LN_SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int blocks = 0;
+  for (int i = 0; i < L.njobs; ++i) {
+    ln_finish_job(L.job[i], &L.map[i]);
+    blocks += L.job[i].blocks;
+  }
+  line_kernel<OP><<<unsigned(blocks), LN_LINES, LN_SMEM, st>>>(L);
+  note_launch();
+  return cudaGetLastError();
+}
+
+inline LineJob ln_job(const double* X, int64_t ld, int64_t nlines, int64_t len, bool by_rows, int op) {
+  LineJob j{};
+  j.X = X;
+  j.ld = ld;
+  j.nlines = nlines;
+  j.len = len;
+  j.pair_end = 2 * (len / 2);
+  j.by_rows = by_rows ? 1 : 0;
+  j.op = op;
+  j.scale_sel = -1;
+  return j;
+}
+
+// ||X||_inf of one or two matrices in one launch; out[i] zeroed here, then max-reduced.
+inline cudaError_t launch_norms(const double* X0, int64_t r0, int64_t c0, const double* X1, int64_t r1, int64_t c1,
+                                unsigned long long* out, cudaStream_t st) {
+  const int n = X1 ? 2 : 1;
+  cudaError_t e = cudaMemsetAsync(out, 0, n * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  LineLaunch L{};
+  L.njobs = n;
+  L.job[0] = ln_job(X0, c0, r0, c0, true, LN_ABS);
+  L.job[0].out_max = out;
+  if (X1) {
+    L.job[1] = ln_job(X1, c1, r1, c1, true, LN_ABS);
+    L.job[1].out_max = out + 1;
+  }
+  return launch_lines<LN_ABS>(L, st);
+}
+
+// Winograd y (rows of A) and z (columns of B); optionally on the exact scaled copies
+// As = 2^lambda A, Bs = 2^-lambda B, which are written in the same pass (lambda from norms).
+inline cudaError_t launch_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M,
+                             double* As, double* Bs, const unsigned long long* norms, int* lam_out, double* scale_out,
+                             cudaStream_t st) {
+  LineLaunch L{};
+  L.njobs = 2;
+  L.norms = norms;
+  L.lam_out = lam_out;
+  L.scale_out = scale_out;
+  const bool scaled = As != nullptr;
+  // y: rows of A (stream the whole row when the copy needs the odd column too)
+  L.job[0] = ln_job(A, P, N, scaled ? P : 2 * (P / 2), true, LN_PAIRS);
+  L.job[0].pair_end = 2 * (P / 2);
+  L.job[0].out = y;
+  // z: columns of B (rows 0 .. 2 gamma - 1, or all P rows for the copy)
+  L.job[1] = ln_job(B, M, M, scaled ? P : 2 * (P / 2), false, LN_PAIRS);
+  L.job[1].pair_end = 2 * (P / 2);
+  L.job[1].out = z;
+  if (scaled) {
+    L.job[0].copy = As;
+    L.job[0].scale_sel = 0;
+    L.job[1].copy = Bs;
+    L.job[1].scale_sel = 1;
+  }
+  return launch_lines<LN_PAIRS>(L, st);
+}
+
+}  // namespace mmk

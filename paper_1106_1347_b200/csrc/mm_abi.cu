@@ -170,22 +170,11 @@ int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_
   double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(P) * 8));
   cudaStream_t st = S(stream);
   cudaError_t e = cudaSuccess;
-  const unsigned long long* nrm = norms;
-  if (norms_device) {
-    nrm = reinterpret_cast<const unsigned long long*>(norms_device);  // same 8 bytes, read as bit patterns
-  } else {
-    e = mmk::launch_norm_inf(A, N, P, norms, st);
-    if (e == cudaSuccess) e = mmk::launch_norm_inf(B, P, M, norms + 1, st);
-  }
-  if (e == cudaSuccess) {
-    mmk::lambda_kernel<<<1, 32, 0, st>>>(nrm, lam, scale);
-    mmk::note_launch();
-    e = cudaGetLastError();
-  }
-  // MultiplyWithScalar: the exact copies 2^lambda A and 2^-lambda B
-  if (e == cudaSuccess) e = mmk::launch_scale_copy(A, As, N * P, scale, 0, sms, st);
-  if (e == cudaSuccess) e = mmk::launch_scale_copy(B, Bs, P * M, scale, 1, sms, st);
-  if (e == cudaSuccess) e = mmk::launch_winograd(As, Bs, C, y, z, N, P, M, st, sms);
+  // K4 norms -> lambda + exact copies 2^lambda A, 2^-lambda B + their y, z -> pair sums.
+  // With norms_device the caller's {||A||, ||B||} are used (the same 16 bytes, read as bit patterns).
+  e = mmk::launch_winograd_scaled(A, B, C, N, P, M, norms,
+                                  reinterpret_cast<const unsigned long long*>(norms_device), lam, scale, y, z, As,
+                                  Bs, st, sms);
   if (e == cudaSuccess && lambda_out) {
     e = cudaMemcpyAsync(lambda_out, lam, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

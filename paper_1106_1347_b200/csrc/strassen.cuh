@@ -33,96 +33,115 @@ struct FormArgs {
   int64_t cnt;
 };
 
-template <int VEC>
-__device__ __forceinline__ void ld_quad(const FormArgs& a, const double* base, int64_t r, int64_t c, double* v) {
-  // v[0..VEC) = parent[r][c .. c+VEC) with the zero embedding outside rows_valid x cols_valid
-  const double* p = base + r * a.src_pitch + c;
-  if (VEC == 2 && r < a.rows_valid && c + 1 < a.cols_valid) {
-    double2 w = *reinterpret_cast<const double2*>(p);
+// ---- vector I/O: V = 4 -> 256-bit LDG/STG (sm_100a), V = 2 -> 128-bit, V = 1 -> scalar
+template <int V>
+__device__ __forceinline__ void ldv(const double* p, double* v) {
+  if (V == 4) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+  } else if (V == 2) {
+    const double2 w = __ldg(reinterpret_cast<const double2*>(p));
     v[0] = w.x;
     v[1] = w.y;
   } else {
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) v[e] = (r < a.rows_valid && c + e < a.cols_valid) ? p[e] : 0.0;
+    v[0] = __ldg(p);
   }
 }
-
-template <int VEC>
-__device__ __forceinline__ void st_vec(double* p, const double* v) {
-  if (VEC == 2) {
+template <int V>
+__device__ __forceinline__ void stv(double* p, const double* v) {
+  if (V == 4) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+  } else if (V == 2) {
     *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
   } else {
     p[0] = v[0];
   }
 }
 
-// SIDE 0 = left operands (from A), SIDE 1 = right operands (from B)
-template <int VARIANT, int SIDE, int VEC>
-__global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a) {
-  const int64_t hv = a.h_cols / VEC;
-  const int64_t per_node = a.h_rows * hv;
-  const int64_t total = a.cnt * per_node;
-  const int64_t child_elems = a.h_rows * a.h_cols;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t q = idx / per_node;
-    const int64_t rem = idx - q * per_node;
-    const int64_t i = rem / hv;
-    const int64_t j = (rem - i * hv) * VEC;
-    const double* base = a.src + q * a.src_stride;
-    double x11[VEC], x12[VEC], x21[VEC], x22[VEC];
-    ld_quad<VEC>(a, base, i, j, x11);
-    ld_quad<VEC>(a, base, i, j + a.h_cols, x12);
-    ld_quad<VEC>(a, base, i + a.h_rows, j, x21);
-    ld_quad<VEC>(a, base, i + a.h_rows, j + a.h_cols, x22);
-    double o[7][VEC];
+// v[0..V) = parent[r][c .. c+V) with the zero embedding of P:286 outside rows_valid x cols_valid
+template <int V>
+__device__ __forceinline__ void ld_quad(const FormArgs& a, const double* base, int64_t r, int64_t c, double* v) {
+  const double* p = base + r * a.src_pitch + c;
+  if (r < a.rows_valid && c + V <= a.cols_valid) {
+    ldv<V>(p, v);
+  } else {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      if (VARIANT == SV_NAIV) {
-        if (SIDE == 0) {              // P:271-277, left factors
-          o[0][e] = dadd(x11[e], x22[e]);  // H1: A11 + A22
-          o[1][e] = dadd(x21[e], x22[e]);  // H2: A21 + A22
-          o[2][e] = x11[e];                // H3: A11
-          o[3][e] = x22[e];                // H4: A22
-          o[4][e] = dadd(x11[e], x12[e]);  // H5: A11 + A12
-          o[5][e] = dsub(x21[e], x11[e]);  // H6: A21 - A11
-          o[6][e] = dsub(x12[e], x22[e]);  // H7: A12 - A22
-        } else {                      // right factors
-          o[0][e] = dadd(x11[e], x22[e]);  // H1: B11 + B22
-          o[1][e] = x11[e];                // H2: B11
-          o[2][e] = dsub(x12[e], x22[e]);  // H3: B12 - B22
-          o[3][e] = dsub(x21[e], x11[e]);  // H4: B21 - B11
-          o[4][e] = x22[e];                // H5: B22
-          o[5][e] = dadd(x11[e], x12[e]);  // H6: B11 + B12
-          o[6][e] = dadd(x21[e], x22[e]);  // H7: B21 + B22
-        }
-      } else {
-        if (SIDE == 0) {
-          const double a1 = dsub(x11[e], x21[e]);  // A1 = A11 - A21
-          const double a2 = dsub(x22[e], a1);      // A2 = A22 - A1
-          o[0][e] = x11[e];                        // H1: A11
-          o[1][e] = x12[e];                        // H2: A12
-          o[2][e] = a2;                            // H3: A2
-          o[3][e] = dadd(x21[e], x22[e]);          // H4: A21 + A22
-          o[4][e] = a1;                            // H5: A1
-          o[5][e] = dsub(x12[e], a2);              // H6: A12 - A2
-          o[6][e] = x22[e];                        // H7: A22
+    for (int e = 0; e < V; ++e) v[e] = (r < a.rows_valid && c + e < a.cols_valid) ? p[e] : 0.0;
+  }
+}
+
+// Work mapping of the add/sub kernels: a "row unit" is one row of one node's quadrant; 2^TPRS
+// threads sweep a row unit with V-wide vectors (consecutive threads -> consecutive vectors,
+// so every warp access is a contiguous, fully used run of sectors), 256 >> TPRS row units per
+// block, grid-stride over all cnt * h_rows units.  Index arithmetic is once per row unit.
+
+// SIDE 0 = left operands (from A), SIDE 1 = right operands (from B)
+template <int VARIANT, int SIDE, int V>
+__global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
+  const int64_t units = a.cnt * a.h_rows;
+  const int64_t child_elems = a.h_rows * a.h_cols;
+  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* base = a.src + q * a.src_stride;
+    double* d0 = a.dst + (7 * q) * child_elems + i * a.h_cols;
+    for (int64_t j = int64_t(lt) * V; j < a.h_cols; j += step) {
+      double x11[V], x12[V], x21[V], x22[V];
+      ld_quad<V>(a, base, i, j, x11);
+      ld_quad<V>(a, base, i, j + a.h_cols, x12);
+      ld_quad<V>(a, base, i + a.h_rows, j, x21);
+      ld_quad<V>(a, base, i + a.h_rows, j + a.h_cols, x22);
+      double o[7][V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (VARIANT == SV_NAIV) {
+          if (SIDE == 0) {              // P:271-277, left factors
+            o[0][e] = dadd(x11[e], x22[e]);  // H1: A11 + A22
+            o[1][e] = dadd(x21[e], x22[e]);  // H2: A21 + A22
+            o[2][e] = x11[e];                // H3: A11
+            o[3][e] = x22[e];                // H4: A22
+            o[4][e] = dadd(x11[e], x12[e]);  // H5: A11 + A12
+            o[5][e] = dsub(x21[e], x11[e]);  // H6: A21 - A11
+            o[6][e] = dsub(x12[e], x22[e]);  // H7: A12 - A22
+          } else {                      // right factors
+            o[0][e] = dadd(x11[e], x22[e]);  // H1: B11 + B22
+            o[1][e] = x11[e];                // H2: B11
+            o[2][e] = dsub(x12[e], x22[e]);  // H3: B12 - B22
+            o[3][e] = dsub(x21[e], x11[e]);  // H4: B21 - B11
+            o[4][e] = x22[e];                // H5: B22
+            o[5][e] = dadd(x11[e], x12[e]);  // H6: B11 + B12
+            o[6][e] = dadd(x21[e], x22[e]);  // H7: B21 + B22
+          }
         } else {
-          const double b1 = dsub(x22[e], x12[e]);  // B1 = B22 - B12
-          const double b2 = dadd(b1, x11[e]);      // B2 = B1 + B11
-          o[0][e] = x11[e];                        // H1: B11
-          o[1][e] = x21[e];                        // H2: B21
-          o[2][e] = b2;                            // H3: B2
-          o[3][e] = dsub(x12[e], x11[e]);          // H4: B12 - B11
-          o[4][e] = b1;                            // H5: B1
-          o[5][e] = x22[e];                        // H6: B22
-          o[6][e] = dsub(x21[e], b2);              // H7: B21 - B2
+          if (SIDE == 0) {
+            const double a1 = dsub(x11[e], x21[e]);  // A1 = A11 - A21
+            const double a2 = dsub(x22[e], a1);      // A2 = A22 - A1
+            o[0][e] = x11[e];                        // H1: A11
+            o[1][e] = x12[e];                        // H2: A12
+            o[2][e] = a2;                            // H3: A2
+            o[3][e] = dadd(x21[e], x22[e]);          // H4: A21 + A22
+            o[4][e] = a1;                            // H5: A1
+            o[5][e] = dsub(x12[e], a2);              // H6: A12 - A2
+            o[6][e] = x22[e];                        // H7: A22
+          } else {
+            const double b1 = dsub(x22[e], x12[e]);  // B1 = B22 - B12
+            const double b2 = dadd(b1, x11[e]);      // B2 = B1 + B11
+            o[0][e] = x11[e];                        // H1: B11
+            o[1][e] = x21[e];                        // H2: B21
+            o[2][e] = b2;                            // H3: B2
+            o[3][e] = dsub(x12[e], x11[e]);          // H4: B12 - B11
+            o[4][e] = b1;                            // H5: B1
+            o[5][e] = x22[e];                        // H6: B22
+            o[6][e] = dsub(x21[e], b2);              // H7: B21 - B2
+          }
         }
       }
-    }
-    double* d0 = a.dst + (7 * q) * child_elems + i * a.h_cols + j;
 #pragma unroll
-    for (int t = 0; t < 7; ++t) st_vec<VEC>(d0 + t * child_elems, o[t]);
+      for (int t = 0; t < 7; ++t) stv<V>(d0 + t * child_elems + j, o[t]);
+    }
   }
 }
 
@@ -134,66 +153,56 @@ struct CombineArgs {
   int64_t h_rows, h_cols, cnt;
 };
 
-template <int VEC>
+template <int V>
 __device__ __forceinline__ void st_quad(const CombineArgs& a, double* base, int64_t r, int64_t c, const double* v) {
   double* p = base + r * a.dst_pitch + c;
-  if (VEC == 2 && r < a.rows_valid && c + 1 < a.cols_valid) {
-    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  if (r < a.rows_valid && c + V <= a.cols_valid) {
+    stv<V>(p, v);
   } else {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e)
+    for (int e = 0; e < V; ++e)
       if (r < a.rows_valid && c + e < a.cols_valid) p[e] = v[e];
   }
 }
 
-template <int VARIANT, int VEC>
-__global__ void __launch_bounds__(256) strassen_combine_kernel(CombineArgs a) {
-  const int64_t hv = a.h_cols / VEC;
-  const int64_t per_node = a.h_rows * hv;
-  const int64_t total = a.cnt * per_node;
+template <int VARIANT, int V>
+__global__ void __launch_bounds__(256) strassen_combine_kernel(CombineArgs a, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
+  const int64_t units = a.cnt * a.h_rows;
   const int64_t child_elems = a.h_rows * a.h_cols;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t q = idx / per_node;
-    const int64_t rem = idx - q * per_node;
-    const int64_t i = rem / hv;
-    const int64_t j = (rem - i * hv) * VEC;
-    const double* h0 = a.H + (7 * q) * child_elems + i * a.h_cols + j;
-    double h[7][VEC];
-#pragma unroll
-    for (int t = 0; t < 7; ++t) {
-      if (VEC == 2) {
-        double2 w = *reinterpret_cast<const double2*>(h0 + t * child_elems);
-        h[t][0] = w.x;
-        h[t][1] = w.y;
-      } else {
-        h[t][0] = h0[t * child_elems];
-      }
-    }
-    double c11[VEC], c12[VEC], c21[VEC], c22[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const double H1 = h[0][e], H2 = h[1][e], H3 = h[2][e], H4 = h[3][e], H5 = h[4][e], H6 = h[5][e],
-                   H7 = h[6][e];
-      if (VARIANT == SV_NAIV) {  // P:279-282, left to right
-        c11[e] = dadd(dsub(dadd(H1, H4), H5), H7);
-        c12[e] = dadd(H3, H5);
-        c21[e] = dadd(H2, H4);
-        c22[e] = dadd(dsub(dadd(H1, H3), H2), H6);
-      } else {
-        const double H8 = dadd(H1, H3);
-        const double H9 = dadd(H8, H4);
-        c11[e] = dadd(H1, H2);
-        c12[e] = dadd(H9, H6);
-        c21[e] = dadd(dadd(H8, H5), H7);
-        c22[e] = dadd(H9, H5);
-      }
-    }
+  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* h0 = a.H + (7 * q) * child_elems + i * a.h_cols;
     double* base = a.dst + q * a.dst_stride;
-    st_quad<VEC>(a, base, i, j, c11);
-    st_quad<VEC>(a, base, i, j + a.h_cols, c12);
-    st_quad<VEC>(a, base, i + a.h_rows, j, c21);
-    st_quad<VEC>(a, base, i + a.h_rows, j + a.h_cols, c22);
+    for (int64_t j = int64_t(lt) * V; j < a.h_cols; j += step) {
+      double h[7][V];
+#pragma unroll
+      for (int t = 0; t < 7; ++t) ldv<V>(h0 + t * child_elems + j, h[t]);
+      double c11[V], c12[V], c21[V], c22[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const double H1 = h[0][e], H2 = h[1][e], H3 = h[2][e], H4 = h[3][e], H5 = h[4][e], H6 = h[5][e],
+                     H7 = h[6][e];
+        if (VARIANT == SV_NAIV) {  // P:279-282, left to right
+          c11[e] = dadd(dsub(dadd(H1, H4), H5), H7);
+          c12[e] = dadd(H3, H5);
+          c21[e] = dadd(H2, H4);
+          c22[e] = dadd(dsub(dadd(H1, H3), H2), H6);
+        } else {
+          const double H8 = dadd(H1, H3);
+          const double H9 = dadd(H8, H4);
+          c11[e] = dadd(H1, H2);
+          c12[e] = dadd(H9, H6);
+          c21[e] = dadd(dadd(H8, H5), H7);
+          c22[e] = dadd(H9, H5);
+        }
+      }
+      st_quad<V>(a, base, i, j, c11);
+      st_quad<V>(a, base, i, j + a.h_cols, c12);
+      st_quad<V>(a, base, i + a.h_rows, j, c21);
+      st_quad<V>(a, base, i + a.h_rows, j + a.h_cols, c22);
+    }
   }
 }
 
@@ -257,52 +266,76 @@ inline bool make_strassen_plan(int64_t N, int64_t P, int64_t M, int levels, Stra
   return true;
 }
 
-inline unsigned grid_for(int64_t work, int sms) {
-  int64_t b = cdiv(work, 256);
-  int64_t cap = int64_t(sms) * 16;  // grid-stride beyond 16 blocks per SM
-  if (b > cap) b = cap;
-  if (b < 1) b = 1;
-  return unsigned(b);
+// threads per row unit: the smallest power of two (32 .. 256) covering the row's vectors
+inline int tpr_shift(int64_t h_cols, int v) {
+  const int64_t vecs = cdiv(h_cols, v);
+  int s = 5;
+  while (s < 8 && (int64_t(1) << s) < vecs) ++s;
+  return s;
 }
 
-template <int VARIANT>
-cudaError_t launch_form_level(int side, const FormArgs& fa, bool vec, int sms, cudaStream_t st) {
-  const int64_t work = fa.cnt * fa.h_rows * (vec ? fa.h_cols / 2 : fa.h_cols);
-  const unsigned g = grid_for(work, sms);
-  if (side == 0) {
-    if (vec) {
-      strassen_form_kernel<VARIANT, 0, 2><<<g, 256, 0, st>>>(fa);
-      note_launch();
-    }
-    else {
-      strassen_form_kernel<VARIANT, 0, 1><<<g, 256, 0, st>>>(fa);
-      note_launch();
-    }
-  } else {
-    if (vec) {
-      strassen_form_kernel<VARIANT, 1, 2><<<g, 256, 0, st>>>(fa);
-      note_launch();
-    }
-    else {
-      strassen_form_kernel<VARIANT, 1, 1><<<g, 256, 0, st>>>(fa);
-      note_launch();
+// vector width usable by every access of a launch: base pointers 8 V-byte aligned, row pitches,
+// node strides and quadrant widths multiples of V
+inline int pick_vec(const void* p0, const void* p1, int64_t pitch, int64_t stride, int64_t h_cols) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p0) | reinterpret_cast<uintptr_t>(p1);
+  for (int v = 4; v > 1; v >>= 1)
+    if ((a & (8 * v - 1)) == 0 && pitch % v == 0 && stride % v == 0 && h_cols % v == 0) return v;
+  return 1;
+}
+
+template <auto KERN>
+inline unsigned grid_for(int64_t units, int tprs, int sms) {
+  static int per_sm = 0;  // resident blocks per SM of this kernel
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KERN, 256, 0) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 4;
     }
   }
+  int64_t b = cdiv(units, int64_t(256 >> tprs));
+  const int64_t cap = int64_t(sms) * per_sm;  // one full wave, grid-stride beyond it
+  if (b > cap) b = cap;
+  return unsigned(b < 1 ? 1 : b);
+}
+
+template <int VARIANT, int SIDE>
+cudaError_t launch_form_side(const FormArgs& fa, int v, int sms, cudaStream_t st) {
+  const int64_t units = fa.cnt * fa.h_rows;
+  const int tprs = tpr_shift(fa.h_cols, v);
+  if (v == 4) {
+    constexpr auto k = strassen_form_kernel<VARIANT, SIDE, 4>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  } else if (v == 2) {
+    constexpr auto k = strassen_form_kernel<VARIANT, SIDE, 2>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  } else {
+    constexpr auto k = strassen_form_kernel<VARIANT, SIDE, 1>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  }
+  note_launch();
   return cudaGetLastError();
 }
 
 template <int VARIANT>
-cudaError_t launch_combine_level(const CombineArgs& ca, bool vec, int sms, cudaStream_t st) {
-  const int64_t work = ca.cnt * ca.h_rows * (vec ? ca.h_cols / 2 : ca.h_cols);
-  const unsigned g = grid_for(work, sms);
-  if (vec) {
-    strassen_combine_kernel<VARIANT, 2><<<g, 256, 0, st>>>(ca);
-    note_launch();
+cudaError_t launch_form_level(int side, const FormArgs& fa, int v, int sms, cudaStream_t st) {
+  return side == 0 ? launch_form_side<VARIANT, 0>(fa, v, sms, st) : launch_form_side<VARIANT, 1>(fa, v, sms, st);
+}
+
+template <int VARIANT>
+cudaError_t launch_combine_level(const CombineArgs& ca, int v, int sms, cudaStream_t st) {
+  const int64_t units = ca.cnt * ca.h_rows;
+  const int tprs = tpr_shift(ca.h_cols, v);
+  if (v == 4) {
+    constexpr auto k = strassen_combine_kernel<VARIANT, 4>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(ca, tprs);
+  } else if (v == 2) {
+    constexpr auto k = strassen_combine_kernel<VARIANT, 2>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(ca, tprs);
+  } else {
+    constexpr auto k = strassen_combine_kernel<VARIANT, 1>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(ca, tprs);
   }
-  else {
-    strassen_combine_kernel<VARIANT, 1><<<g, 256, 0, st>>>(ca);
-    note_launch();
-  }
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -314,7 +347,6 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
     GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
     return launch_dgemm(pr, st, sms);
   }
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   cudaError_t e;
   double* S[2] = {reinterpret_cast<double*>(ws + pl.offS[0]), reinterpret_cast<double*>(ws + pl.offS[1])};
   double* T[2] = {reinterpret_cast<double*>(ws + pl.offT[0]), reinterpret_cast<double*>(ws + pl.offT[1])};
@@ -344,8 +376,8 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
       fa.h_rows = r_l / 2;
       fa.h_cols = c_l / 2;
       fa.cnt = ipow7(l);
-      const bool vec = (fa.h_cols % 2 == 0) && (fa.src_pitch % 2 == 0) && al16(fa.src);
-      e = launch_form_level<VARIANT>(side, fa, vec, sms, st);
+      const int v = pick_vec(fa.src, fa.dst, fa.src_pitch, fa.src_stride, fa.h_cols);
+      e = launch_form_level<VARIANT>(side, fa, v, sms, st);
       if (e != cudaSuccess) return e;
     }
   }
@@ -376,8 +408,8 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
     ca.h_rows = r_l / 2;
     ca.h_cols = c_l / 2;
     ca.cnt = ipow7(l);
-    const bool vec = (ca.h_cols % 2 == 0) && (ca.dst_pitch % 2 == 0) && al16(ca.dst);
-    e = launch_combine_level<VARIANT>(ca, vec, sms, st);
+    const int v = pick_vec(ca.dst, ca.H, ca.dst_pitch, ca.dst_stride, ca.h_cols);
+    e = launch_combine_level<VARIANT>(ca, v, sms, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -8,96 +8,23 @@
 // equals the oracle's or_winograd_original bit for bit -- required, because on ill-scaled
 // inputs (config c3) two equally valid summation orders differ by ~50 in the inf-norm.
 //
-// WinogradScaled runs these same kernels on the copies 2^lambda A and
-// 2^-lambda B made by scale_copy_kernel (MultiplyWithScalar; exact power-of-two
-// scalings, lambda read from device memory written by lambda_kernel -- no host round trip).
+// WinogradScaled runs the pair-sum kernel on the copies 2^lambda A and 2^-lambda B
+// (MultiplyWithScalar; exact power-of-two scalings), which the y/z pass writes while it
+// computes y and z on them; lambda is derived on the device from the two norms -- no host round
+// trip.
 //
 // Kernels:
-//  * winograd_yz_kernel: y (one lane per row of A) and z (one lane per column of B), 32 x 32
-//    tiles streamed through a cp.async ring -- sequential sums, HBM-bound.
+//  * line_kernel<LN_PAIRS> (lines.cuh): y (one lane per row of A) and z (one lane per column of
+//    B), sequential sums streamed by bulk copies, HBM-bound; optionally also the scaled copies.
 //  * winograd_kernel: SimtCfg tiles (below); the pair loop covers columns 0..2*gamma-1 only
 //    (the odd column never enters acc).
 #pragma once
-#include "norm_lambda.cuh"
+#include "lines.cuh"
 #include "simt_tile.cuh"
 
 #include <type_traits>
 
 namespace mmk {
-
-// MultiplyWithScalar: dst = scale[which] * src, elementwise, HBM-bound.
-__global__ void __launch_bounds__(256) scale_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                                                         int64_t n, const double* __restrict__ scale, int which) {
-  const double s = scale[which];
-  if ((reinterpret_cast<uintptr_t>(src) & 15) != 0) {  // 8-byte aligned source: scalar path
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-      dst[i] = dmul(s, src[i]);
-    return;
-  }
-  const int64_t n2 = n / 2;
-  const double2* s2 = reinterpret_cast<const double2*>(src);
-  double2* d2 = reinterpret_cast<double2*>(dst);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
-    double2 v = s2[i];
-    d2[i] = make_double2(dmul(s, v.x), dmul(s, v.y));
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) dst[n - 1] = dmul(s, src[n - 1]);
-}
-
-// ---------------------------------------------------------------- y / z prologue
-// One warp owns 32 lines: 32 rows of A (y) or 32 columns of B (z), streamed through the
-// cp.async line ring of norm_lambda.cuh; each lane accumulates its own line in increasing j
-// (the oracle's order).  HBM-bound: 8 (NP + PM) bytes read.
-// blocks [0, nb_y) compute y for rows [32 b, 32 b + 32); blocks [nb_y, ...) compute z.
-__global__ void __launch_bounds__(LS_LINES) winograd_yz_kernel(const double* __restrict__ A,
-                                                               const double* __restrict__ B, double* __restrict__ y,
-                                                               double* __restrict__ z, int64_t N, int64_t P,
-                                                               int64_t M, int nb_y) {
-  extern __shared__ __align__(16) double ls_smem[];
-  const int lane = threadIdx.x;
-  const bool is_y = int(blockIdx.x) < nb_y;
-  const int64_t l0 = int64_t(is_y ? blockIdx.x : blockIdx.x - nb_y) * LS_LINES;
-  const int64_t kend = 2 * (P / 2);  // the odd column / row never enters y or z
-  const int64_t KT = cdiv(kend, LS_TK);
-  auto load = [&](int64_t kt, int s) {
-    double* t = ls_smem + s * LS_TILE;
-    if (is_y) ls_load_rowlines(t, A, P, l0, kt * LS_TK, N, kend, lane);
-    else ls_load_collines(t, B, M, kt * LS_TK, l0, kend, M, lane);
-  };
-#pragma unroll
-  for (int s = 0; s < LS_STAGES - 1; ++s) {
-    if (s < KT) load(s, s);
-    cp_async_commit();
-  }
-  double acc = 0.0;
-  for (int64_t kt = 0; kt < KT; ++kt) {
-    cp_async_wait<LS_STAGES - 2>();
-    __syncwarp();
-    {
-      const int64_t nk = kt + LS_STAGES - 1;
-      if (nk < KT) load(nk, int(nk % LS_STAGES));
-      cp_async_commit();
-    }
-    const double* t = ls_smem + (kt % LS_STAGES) * LS_TILE;
-    const int64_t rem = kend - kt * LS_TK;
-    const int npairs = int(rem < LS_TK ? rem : LS_TK) / 2;
-    if (is_y) {
-      const double* row = t + lane * LS_ROWPITCH;
-      for (int j = 0; j < npairs; ++j) acc = dadd(acc, dmul(row[2 * j], row[2 * j + 1]));
-    } else {
-      for (int j = 0; j < npairs; ++j)
-        acc = dadd(acc, dmul(t[(2 * j) * LS_COLPITCH + lane], t[(2 * j + 1) * LS_COLPITCH + lane]));
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  const int64_t idx = l0 + lane;
-  if (is_y) {
-    if (idx < N) y[idx] = acc;
-  } else {
-    if (idx < M) z[idx] = acc;
-  }
-}
 
 // ---------------------------------------------------------------- main pair-sum kernel
 // 128 x 64 tiles, 128 threads of 8 x 8 outputs, 2 CTAs per SM; 64 x 64 tiles of 4 x 8 when the
@@ -220,21 +147,6 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
   return cudaGetLastError();
 }
 
-inline cudaError_t launch_winograd_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P,
-                                      int64_t M, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(winograd_yz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS_SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int nb_y = int(cdiv(N, LS_LINES));
-  const int nb_z = int(cdiv(M, LS_LINES));
-  winograd_yz_kernel<<<nb_y + nb_z, LS_LINES, LS_SMEM, st>>>(A, B, y, z, N, P, M, nb_y);
-  note_launch();
-  return cudaGetLastError();
-}
-
 // y, z: device buffers of N and M doubles.
 template <class CF>
 inline cudaError_t launch_winograd_main(const double* A, const double* B, double* C, const double* y,
@@ -246,11 +158,11 @@ inline cudaError_t launch_winograd_main(const double* A, const double* B, double
   return launch_winograd_t<CF, 1, 1, 1>(A, B, C, y, z, N, P, M, st);
 }
 
+// the pair-sum kernel with the tile configuration chosen by problem size (y, z already computed)
 template <class CF = void>
-inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
-                                   int64_t P, int64_t M, cudaStream_t st, int sms = 148) {
-  cudaError_t e = launch_winograd_yz(A, B, y, z, N, P, M, st);
-  if (e != cudaSuccess) return e;
+inline cudaError_t launch_winograd_pairs(const double* A, const double* B, double* C, const double* y,
+                                         const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st,
+                                         int sms = 148) {
   if (!std::is_void<CF>::value)
     return launch_winograd_main<typename std::conditional<std::is_void<CF>::value, WinogradDefault, CF>::type>(
         A, B, C, y, z, N, P, M, st);
@@ -259,13 +171,27 @@ inline cudaError_t launch_winograd(const double* A, const double* B, double* C, 
   return launch_winograd_main<WinogradSmall>(A, B, C, y, z, N, P, M, st);
 }
 
-inline cudaError_t launch_scale_copy(const double* src, double* dst, int64_t n, const double* scale, int which,
-                                     int sms, cudaStream_t st) {
-  int64_t blocks = cdiv(n / 2 + 1, 256);
-  if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
-  scale_copy_kernel<<<unsigned(blocks), 256, 0, st>>>(src, dst, n, scale, which);
-  note_launch();
-  return cudaGetLastError();
+template <class CF = void>
+inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
+                                   int64_t P, int64_t M, cudaStream_t st, int sms = 148) {
+  cudaError_t e = launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+  if (e != cudaSuccess) return e;
+  return launch_winograd_pairs<CF>(A, B, C, y, z, N, P, M, st, sms);
+}
+
+// WinogradScaled: norms (one launch, K4) -> lambda, exact copies 2^lambda A and
+// 2^-lambda B, and their y / z (one fused launch) -> pair sums on the copies.  C is not rescaled
+// (P:216).  Norms are device {||A||, ||B||} bit patterns: given (e.g. the distributed driver's
+// all-reduced ||A||) or, when given == nullptr, computed into `norms`.
+inline cudaError_t launch_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P,
+                                          int64_t M, unsigned long long* norms, const unsigned long long* given,
+                                          int* lam, double* scale, double* y, double* z, double* As, double* Bs,
+                                          cudaStream_t st, int sms = 148) {
+  cudaError_t e = cudaSuccess;
+  if (!given) e = launch_norms(A, N, P, B, P, M, norms, st);
+  if (e == cudaSuccess) e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st);
+  if (e == cudaSuccess) e = launch_winograd_pairs(As, Bs, C, y, z, N, P, M, st, sms);
+  return e;
 }
 
 }  // namespace mmk

@@ -342,3 +342,39 @@ def test_host_matmul_pipelined_bitwise():
             out = torch.empty((515, 257), dtype=torch.float64).pin_memory()
             C = mm.matmul(hA, hB, name, out=out, row_blocks=rb)
             assert np.array_equal(C.numpy(), ref), (name, rb)
+
+
+def _unaligned(x: np.ndarray) -> torch.Tensor:
+    """A contiguous CUDA copy of x whose data pointer is 8 (not 16) bytes aligned: exercises the
+    8-byte fallback loaders (cp.async 8 B instead of bulk / 16-byte copies)."""
+    buf = torch.empty(x.size + 1, dtype=torch.float64, device=DEV)
+    t = buf[1:].view(x.shape)
+    t.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+    assert t.data_ptr() % 16 == 8 and t.is_contiguous()
+    return t
+
+
+@pytest.mark.parametrize("shape", [(67, 46, 52), (130, 64, 96), (33, 1, 40)])
+def test_unaligned_operands_bitwise(shape):
+    N, P, M = shape
+    A, B = workload.custom(N, P, M, seed=N + 7 * P + 13 * M)
+    A = A * 1e3
+    refs = {"naive": oracle.naive_fma(A, B), "kahan": oracle.naive_kahan(A, B),
+            "winograd": oracle.winograd_original(A, B), "winograd_scaled": oracle.winograd_scaled(A, B)[0]}
+    for dA, dB in ((_unaligned(A), dev(B)), (dev(A), _unaligned(B)), (_unaligned(A), _unaligned(B))):
+        for name, ref in refs.items():
+            assert np.array_equal(host(run(name, dA, dB)), ref), (name, shape)
+        for name, v in (("strassen", 0), ("strassen_winograd", 1)):
+            d, pad = plan_pad(N, P, M, 2)
+            assert np.array_equal(host(run(name, dA, dB, 2)),
+                                  oracle.strassen(v, A, B, levels=d, pad=pad, base=oracle.BASE_FMA)), name
+        assert mm.norm_inf(dA).item() == oracle.norm_inf(A)
+        assert mm.norm_inf(dB).item() == oracle.norm_inf(B)
+
+
+def test_norm_inf_many_shapes():
+    """Row counts around the 32-line blocks, even and odd widths, tiles of 32 columns +- 1."""
+    for rows in (1, 31, 32, 33, 95, 300):
+        for cols in (1, 2, 31, 32, 33, 64, 65, 130):
+            X = workload.custom(rows, cols, 1, rows * 1000 + cols)[0] * 7.0
+            assert mm.norm_inf(dev(X)).item() == oracle.norm_inf(X), (rows, cols)
