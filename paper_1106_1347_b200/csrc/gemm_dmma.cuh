@@ -234,7 +234,7 @@ inline cudaError_t launch_dgemm_cfg(const GemmProblem& pr, cudaStream_t st) {
 }
 
 // tile configuration by problem size (the per-entry arithmetic is identical for both)
-inline cudaError_t launch_dgemm(const GemmProblem& pr, cudaStream_t st, int sms = 148) {
+inline cudaError_t launch_dgemm_cpasync(const GemmProblem& pr, cudaStream_t st, int sms = 148) {
   const int64_t tiles = cdiv(pr.N, GemmDefault::BM) * cdiv(pr.M, GemmDefault::BN) * pr.batch;
   if (tiles >= 4 * int64_t(sms)) return launch_dgemm_cfg<GemmDefault>(pr, st);
   return launch_dgemm_cfg<GemmSmall>(pr, st);

@@ -9,7 +9,7 @@
 #include <cstring>
 
 #include "common.cuh"
-#include "gemm_dmma.cuh"
+#include "gemm_tma.cuh"
 #include "kahan.cuh"
 #include "norm_lambda.cuh"
 #include "strassen.cuh"

@@ -16,7 +16,7 @@
 // All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
 #pragma once
 #include "common.cuh"
-#include "gemm_dmma.cuh"
+#include "gemm_tma.cuh"
 
 namespace mmk {
 

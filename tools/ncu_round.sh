@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 echo "launch list rc=$?"
 for M in naive kahan winograd; do
   QB="python tools/quick_bench.py --methods $M --reps 1"
-  case $M in naive) K=dgemm_dmma;; kahan) K=kahan_gemm;; winograd) K=winograd_kernel;; esac
+  case $M in naive) K=dgemm_tma;; kahan) K=kahan_gemm;; winograd) K=winograd_kernel;; esac
   $QB > $OUT/plain_qb_$M.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o $OUT/full_$M $QB > $OUT/ncu_full_$M.log 2>&1
   echo "full $M rc=$?"
@@ -19,6 +19,6 @@ done
 QB="python tools/quick_bench.py --methods winograd_scaled,strassen_winograd --reps 1"
 $QB > $OUT/plain_qb_hbm.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
-    --clock-control none -k regex:"strassen_form|strassen_combine|norm_inf|scale_copy|winograd_yz" --csv \
+    --clock-control none -k regex:"strassen_form|strassen_combine|line_kernel" --csv \
     --log-file $OUT/hbm_kernels.csv $QB > $OUT/ncu_hbm.log 2>&1
 echo "hbm rc=$?"

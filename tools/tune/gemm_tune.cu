@@ -6,7 +6,7 @@
 #include <cstring>
 #include <vector>
 
-#include "../../paper_1106_1347_b200/csrc/gemm_dmma.cuh"
+#include "../../paper_1106_1347_b200/csrc/gemm_tma.cuh"
 
 using namespace mmk;
 
@@ -25,12 +25,13 @@ __global__ void cmp(const double* a, const double* b, int64_t n, unsigned long l
     if (a[i] != b[i]) atomicAdd(bad, 1ull);
 }
 
-template <class CF>
+template <class CF, bool TMA = false>
 void run(const char* name, const double* A, const double* B, double* C, const double* Cref, int64_t n, int reps,
          unsigned long long* bad) {
   GemmProblem pr{A, B, C, n, n, n, n, n, n, 0, 0, 0, 1};
   cudaMemset(C, 0, n * n * 8);
-  if (launch_dgemm_cfg<CF>(pr, 0) != cudaSuccess) {
+  auto go = [&]() { return TMA ? launch_dgemm_tma<CF>(pr, 0) : launch_dgemm_cfg<CF>(pr, 0); };
+  if (go() != cudaSuccess) {
     printf("{\"cfg\":\"%s\",\"error\":\"%s\"}\n", name, cudaGetErrorString(cudaGetLastError()));
     return;
   }
@@ -39,7 +40,7 @@ void run(const char* name, const double* A, const double* B, double* C, const do
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) launch_dgemm_cfg<CF>(pr, 0);
+  for (int r = 0; r < reps; ++r) go();
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -69,11 +70,13 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
-  run<GemmCfg<128, 64, 2, 2, 4, 2>>("128x64_w2x2_s4_2cta", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<128, 64, 2, 2, 2, 2, 32>>("128x64_w2x2_s2_2cta_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<128, 64, 2, 2, 3, 1, 32>>("128x64_w2x2_s3_1cta_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 3, 3, 32>>("64x64_w2x2_s3_3cta_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<128, 128, 2, 4, 3, 1, 32>>("128x128_w2x4_s3_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 128, 1, 4, 2, 2, 32>>("64x128_w1x4_s2_2cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 2, 2, 4, 2>>("cpasync_128x64_w2x2_s4_2cta", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 3, 4>, true>("tma_64x64_w2x2_s3_4cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 2, 6>, true>("tma_64x64_w2x2_s2_6cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 128, 2, 2, 3, 3>, true>("tma_64x128_w2x2_s3_3cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 4, 2, 4, 2>, true>("tma_128x64_w4x2_s4_2cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 4, 2, 3, 3>, true>("tma_128x64_w4x2_s3_3cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta_again", A, B, C, R, n, reps, bad);
   return 0;
 }
