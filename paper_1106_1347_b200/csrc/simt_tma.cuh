@@ -1,0 +1,317 @@
+// simt_tma.cuh -- TMA-fed main loops of the FP64 SIMT kernels: K2 Kahan and
+// K3 Winograd pair sums, for operands a tensor map can describe (16-byte aligned,
+// even pitches: P and M even).  Other operands use the cp.async kernels of kahan.cuh /
+// winograd.cuh.  Measured at 8192^3 (profiles/r01/simt_tune_tma.jsonl): Winograd 65.6 ms vs
+// 67.4 ms with cp.async -> the product path; Kahan 161.7 ms vs 157.8 ms -> kept for the tuning
+// harness only (the swizzled address arithmetic costs more than the barriers it removes).
+// Per output entry the arithmetic and its order are exactly those kernels' (and the
+// oracle's): only the operand staging differs, so results are bitwise identical.
+//
+//  * A tile = one TMA box [BM rows][16 k], B tile = BN/16 boxes [16 k][16 columns], 128-byte
+//    swizzle (16-byte chunk q of box row r at chunk q ^ (r % 8)).  Thread (ty, tx) reads rows
+//    ty + TYM i of A (4 consecutive rows per warp -> 4 distinct chunks, broadcast over tx) and
+//    the column pairs 2 tx + 16 c of B (box c, chunk tx -> 8 distinct chunks): conflict free.
+//  * One thread issues the copies into a STAGES-deep ring with per-stage full (expect_tx) and
+//    empty (one arrival per warp) mbarriers: no CTA-wide barrier in the main loop.
+//  * TMA zero-fills out-of-range rows/columns; the Kahan k-loop still stops exactly at P (a
+//    zero term is not a no-op for the compensated update) and Winograd's pair loop ends at
+//    gamma = P/2 (P is even on this path).
+#pragma once
+#include "simt_tile.cuh"
+#include "tma.cuh"
+
+namespace mmk {
+
+struct SimtTmaArgs {
+  CUtensorMap mapA, mapB;
+  const double* A;  // for Winograd's epilogue (odd P never takes this path, kept for symmetry)
+  const double* B;
+  double* C;
+  const double* y;
+  const double* z;
+  int64_t N, P, M;
+};
+
+template <class CF>
+struct SimtTmaLayout {
+  static constexpr int A_TILE = CF::BM * 16, B_TILE = 16 * CF::BN;
+  static constexpr unsigned STAGE_BYTES = unsigned(A_TILE + B_TILE) * 8u;
+  static constexpr size_t SMEM = 1024 + size_t(CF::STAGES) * STAGE_BYTES + 2 * CF::STAGES * 8;
+  static_assert(CF::TXN == 8, "a warp's 8 column pairs must fill one 16-column TMA box row");
+  static_assert(CF::BK == 16, "tiles of 16 k");
+};
+
+// A[row][k] in the swizzled [BM][16] box
+__device__ __forceinline__ int sw_a(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7))) << 1) + (k & 1); }
+// B[k][2 tx + 16 c .. +1] (a 16-byte pair) in box c of [16][16]
+__device__ __forceinline__ int sw_b(int k, int tx, int c) { return c * 256 + k * 16 + ((tx ^ (k & 7)) << 1); }
+
+template <class CF>
+struct SimtPipe {
+  using LY = SimtTmaLayout<CF>;
+  double* As_base;
+  double* Bs_base;
+  uint64_t* full;
+  uint64_t* empty;
+  int m0, n0, KT;
+
+  __device__ __forceinline__ void init(unsigned char* raw, int m0_, int n0_, int KT_) {
+    double* sm = reinterpret_cast<double*>(raw + ((1024 - (smem_u32(raw) & 1023)) & 1023));
+    As_base = sm;
+    Bs_base = sm + CF::STAGES * LY::A_TILE;
+    full = reinterpret_cast<uint64_t*>(Bs_base + CF::STAGES * LY::B_TILE);
+    empty = full + CF::STAGES;
+    m0 = m0_;
+    n0 = n0_;
+    KT = KT_;
+  }
+  __device__ __forceinline__ void issue(const SimtTmaArgs& a, int kt, int s) {
+    mbar_arrive_expect_tx(full + s, LY::STAGE_BYTES);
+    tma_load_2d(As_base + s * LY::A_TILE, &a.mapA, kt * 16, m0, full + s);
+#pragma unroll
+    for (int c = 0; c < CF::BN / 16; ++c)
+      tma_load_2d(Bs_base + s * LY::B_TILE + c * 256, &a.mapB, n0 + 16 * c, kt * 16, full + s);
+  }
+  // barriers + prologue; every thread calls it
+  __device__ __forceinline__ void start(const SimtTmaArgs& a) {
+    if (threadIdx.x == 0) {
+      tma_prefetch_desc(&a.mapA);
+      tma_prefetch_desc(&a.mapB);
+      for (int s = 0; s < CF::STAGES; ++s) {
+        mbar_init(full + s, 1);
+        mbar_init(empty + s, CF::THREADS / 32);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int s = 0; s < CF::STAGES && s < KT; ++s) issue(a, s, s);
+  }
+  // top of tile kt: refill the stage of tile kt-1, then wait for tile kt; returns its stage
+  __device__ __forceinline__ int acquire(const SimtTmaArgs& a, int kt) {
+    if (threadIdx.x == 0 && kt >= 1) {
+      const int kp = kt - 1 + CF::STAGES;
+      if (kp < KT) {
+        const int sp = (kt - 1) % CF::STAGES;
+        mbar_wait(empty + sp, unsigned(((kt - 1) / CF::STAGES) & 1));
+        issue(a, kp, sp);
+      }
+    }
+    const int s = kt % CF::STAGES;
+    mbar_wait(full + s, unsigned((kt / CF::STAGES) & 1));
+    return s;
+  }
+  __device__ __forceinline__ void release(int s) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
+  }
+};
+
+// ---------------------------------------------------------------- K2 Kahan, TMA-fed (tuning harness)
+template <class CF, int CV>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const __grid_constant__ SimtTmaArgs a) {
+  using LY = SimtTmaLayout<CF>;
+  extern __shared__ __align__(1024) unsigned char k_raw[];
+  const int tid = threadIdx.x, tx = tid % CF::TXN, ty = tid / CF::TXN;
+  int64_t m0, n0;
+  simt_tile_coords(a.N, a.M, CF::BM, CF::BN, m0, n0);
+  SimtPipe<CF> pp;
+  pp.init(k_raw, int(m0), int(n0), int(cdiv(a.P, 16)));
+  pp.start(a);
+
+  double sum[CF::TM][CF::TN], err[CF::TM][CF::TN];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j) sum[i][j] = err[i][j] = 0.0;
+
+  auto step = [&](const double* As, const double* Bs, int kk) {
+    double av[CF::TM], bv[CF::TN];
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) av[i] = As[sw_a(simt_row<CF>(ty, i), kk)];
+#pragma unroll
+    for (int c = 0; c < CF::TN / 2; ++c) {
+      const double2 v = *reinterpret_cast<const double2*>(Bs + sw_b(kk, tx, c));
+      bv[2 * c] = v.x;
+      bv[2 * c + 1] = v.y;
+    }
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j) {  // the update of P:122-132, every op separately rounded
+        const double x = dmul(av[i], bv[j]);
+        double e = dadd(err[i][j], x);
+        const double t = dadd(sum[i][j], e);
+        e = dadd(dsub(sum[i][j], t), e);
+        sum[i][j] = t;
+        err[i][j] = e;
+      }
+  };
+
+#pragma unroll 1
+  for (int kt = 0; kt < pp.KT; ++kt) {
+    const int s = pp.acquire(a, kt);
+    const double* As = pp.As_base + s * LY::A_TILE;
+    const double* Bs = pp.Bs_base + s * LY::B_TILE;
+    const int64_t k0 = int64_t(kt) * 16;
+    if (k0 + 16 <= a.P) {
+#pragma unroll 4
+      for (int kk = 0; kk < 16; ++kk) step(As, Bs, kk);
+    } else {
+      const int kmax = int(a.P - k0);  // stop exactly at P
+      for (int kk = 0; kk < kmax; ++kk) step(As, Bs, kk);
+    }
+    pp.release(s);
+  }
+
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i) {
+    const int64_t row = m0 + simt_row<CF>(ty, i);
+    if (row >= a.N) continue;
+#pragma unroll
+    for (int c = 0; c < CF::TN / 2; ++c) {
+      const int64_t col = n0 + 2 * tx + 2 * CF::TXN * c;
+      if (CV == 2 && col + 1 < a.M) {
+        *reinterpret_cast<double2*>(a.C + row * a.M + col) = make_double2(sum[i][2 * c], sum[i][2 * c + 1]);
+      } else {
+        if (col < a.M) a.C[row * a.M + col] = sum[i][2 * c];
+        if (col + 1 < a.M) a.C[row * a.M + col + 1] = sum[i][2 * c + 1];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K3 Winograd pair sums, TMA-fed (P even)
+template <class CF, int CV>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(const __grid_constant__ SimtTmaArgs a) {
+  using LY = SimtTmaLayout<CF>;
+  constexpr int TM = CF::TM, TN = CF::TN;
+  extern __shared__ __align__(1024) unsigned char w_raw[];
+  const int tid = threadIdx.x, tx = tid % CF::TXN, ty = tid / CF::TXN;
+  int64_t m0, n0;
+  simt_tile_coords(a.N, a.M, CF::BM, CF::BN, m0, n0);
+  SimtPipe<CF> pp;
+  pp.init(w_raw, int(m0), int(n0), int(cdiv(a.P, 16)));  // P even: 2 gamma = P
+  pp.start(a);
+
+  double acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+
+#pragma unroll 1
+  for (int kt = 0; kt < pp.KT; ++kt) {
+    const int s = pp.acquire(a, kt);
+    const double* As = pp.As_base + s * LY::A_TILE;
+    const double* Bs = pp.Bs_base + s * LY::B_TILE;
+    // a zero-filled pair past P adds (0+0)(0+0) = +0 to acc, which leaves acc unchanged
+    // (acc starts at +0 and can never become -0), so the last tile needs no guard
+#pragma unroll 2
+    for (int jp = 0; jp < 8; ++jp) {
+      double a0[TM], a1[TM], b0[TN], b1[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(As + sw_a(simt_row<CF>(ty, i), 2 * jp));
+        a0[i] = v.x;
+        a1[i] = v.y;
+      }
+#pragma unroll
+      for (int c = 0; c < TN / 2; ++c) {
+        const double2 u = *reinterpret_cast<const double2*>(Bs + sw_b(2 * jp, tx, c));
+        const double2 w = *reinterpret_cast<const double2*>(Bs + sw_b(2 * jp + 1, tx, c));
+        b0[2 * c] = u.x;
+        b0[2 * c + 1] = u.y;
+        b1[2 * c] = w.x;
+        b1[2 * c + 1] = w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
+    }
+    pp.release(s);
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t row = m0 + simt_row<CF>(ty, i);
+    if (row >= a.N) continue;
+    const double yi = a.y[row];
+#pragma unroll
+    for (int c = 0; c < TN / 2; ++c) {
+      const int64_t col = n0 + 2 * tx + 2 * CF::TXN * c;
+      double out[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t cc = col + e;
+        out[e] = cc < a.M ? dsub(dsub(acc[i][2 * c + e], yi), a.z[cc]) : 0.0;  // (acc - y_i) - z_k
+      }
+      if (CV == 2 && col + 1 < a.M) {
+        *reinterpret_cast<double2*>(a.C + row * a.M + col) = make_double2(out[0], out[1]);
+      } else {
+        if (col < a.M) a.C[row * a.M + col] = out[0];
+        if (col + 1 < a.M) a.C[row * a.M + col + 1] = out[1];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+inline bool simt_tma_ok(const double* A, const double* B, int64_t N, int64_t P, int64_t M) {
+  return tma_ok(A, P) && tma_ok(B, M) && N <= INT32_MAX && P <= INT32_MAX && M <= INT32_MAX;
+}
+
+template <auto KERN, int THREADS, size_t SMEM>
+inline cudaError_t launch_simt_tma_t_(const SimtTmaArgs& args, unsigned grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  KERN<<<grid, THREADS, SMEM, st>>>(args);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <class CF>
+inline bool simt_tma_args(SimtTmaArgs& args, const double* A, const double* B, double* C, int64_t N, int64_t P,
+                          int64_t M) {
+  args.A = A;
+  args.B = B;
+  args.C = C;
+  args.N = N;
+  args.P = P;
+  args.M = M;
+  return tma_encode_2d(&args.mapA, A, N, P, P, CF::BM, 16, true) &&
+         tma_encode_2d(&args.mapB, B, P, M, M, 16, 16, true);
+}
+
+template <class CF>
+inline cudaError_t launch_kahan_tma(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                                    cudaStream_t st) {
+  using LY = SimtTmaLayout<CF>;
+  SimtTmaArgs args{};
+  if (!simt_tma_args<CF>(args, A, B, C, N, P, M)) return cudaErrorInvalidValue;
+  const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
+  const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
+  return cv ? launch_simt_tma_t_<kahan_tma_kernel<CF, 2>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<kahan_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
+}
+
+template <class CF>
+inline cudaError_t launch_winograd_pairs_tma(const double* A, const double* B, double* C, const double* y,
+                                             const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st) {
+  using LY = SimtTmaLayout<CF>;
+  SimtTmaArgs args{};
+  if (!simt_tma_args<CF>(args, A, B, C, N, P, M)) return cudaErrorInvalidValue;
+  args.y = y;
+  args.z = z;
+  const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
+  const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
+  return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<winograd_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
+}
+
+}  // namespace mmk

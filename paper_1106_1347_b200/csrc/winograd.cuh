@@ -21,6 +21,7 @@
 #pragma once
 #include "lines.cuh"
 #include "simt_tile.cuh"
+#include "simt_tma.cuh"
 
 #include <type_traits>
 
@@ -31,6 +32,8 @@ namespace mmk {
 // big tiles would leave SMs idle (tools/tune/simt_tune.cu, profiles/r01/simt_tune*.jsonl)
 using WinogradDefault = SimtCfg<128, 64, 8, 8, 3, 2>;
 using WinogradSmall = SimtCfg<64, 64, 4, 8, 3, 2>;
+// TMA-fed main loop (simt_tma.cuh) for 16-byte aligned operands with P, M even: 4 stages
+using WinogradTma = SimtCfg<128, 64, 8, 8, 4, 2>;
 
 // The tiles are loaded with kend = 2*gamma: columns/rows >= 2*gamma are zero-filled, so the
 // odd column never enters acc.  A zero-filled pair adds (0+0)(0+0) = +0 to acc, which leaves
@@ -167,7 +170,10 @@ inline cudaError_t launch_winograd_pairs(const double* A, const double* B, doubl
     return launch_winograd_main<typename std::conditional<std::is_void<CF>::value, WinogradDefault, CF>::type>(
         A, B, C, y, z, N, P, M, st);
   const int64_t big_tiles = cdiv(N, WinogradDefault::BM) * cdiv(M, WinogradDefault::BN);
-  if (big_tiles >= 2 * int64_t(sms)) return launch_winograd_main<WinogradDefault>(A, B, C, y, z, N, P, M, st);
+  if (big_tiles >= 2 * int64_t(sms)) {
+    if (simt_tma_ok(A, B, N, P, M)) return launch_winograd_pairs_tma<WinogradTma>(A, B, C, y, z, N, P, M, st);
+    return launch_winograd_main<WinogradDefault>(A, B, C, y, z, N, P, M, st);
+  }
   return launch_winograd_main<WinogradSmall>(A, B, C, y, z, N, P, M, st);
 }
 

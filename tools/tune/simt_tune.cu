@@ -77,6 +77,18 @@ void wino(const char* name, Ctx& c, bool first) {
   if (first) cudaMemcpy(c.R, c.C, c.n * c.n * 8, cudaMemcpyDeviceToDevice);
 }
 
+template <class CF>
+void kahan_tma(const char* name, Ctx& c) {
+  timeit("kahan", name, CF::THREADS, SimtTmaLayout<CF>::SMEM, c, c.R,
+         [&] { launch_kahan_tma<CF>(c.A, c.B, c.C, c.n, c.n, c.n, 0); }, 5.0);
+}
+template <class CF>
+void wino_tma(const char* name, Ctx& c) {
+  timeit("winograd", name, CF::THREADS, SimtTmaLayout<CF>::SMEM, c, c.R, [&] {
+    launch_yz(c.A, c.B, c.y, c.z, c.n, c.n, c.n, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+    launch_winograd_pairs_tma<CF>(c.A, c.B, c.C, c.y, c.z, c.n, c.n, c.n, 0);
+  }, 2.0);
+}
 int main(int argc, char** argv) {
   Ctx c;
   c.n = argc > 1 ? atoll(argv[1]) : 8192;
@@ -91,17 +103,17 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB>
-  wino<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, true);
-  wino<SimtCfg<64, 64, 4, 8, 4, 2>>("64x64_t4x8_s4_2cta", c, false);
-  wino<SimtCfg<64, 128, 8, 8, 3, 2>>("64x128_t8x8_s3_2cta", c, false);
-  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("128x64_t8x8_s3_2cta", c, false);
-  wino<SimtCfg<64, 64, 8, 4, 3, 2>>("64x64_t8x4_s3_2cta", c, false);
-  wino<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
-  wino<SimtCfg<64, 64, 8, 8, 3, 4>>("64x64_t8x8_s3_4cta", c, false);
-  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, true);
-  kahan<SimtCfg<64, 64, 4, 8, 4, 2>>("64x64_t4x8_s4_2cta", c, false);
-  kahan<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
-  kahan<SimtCfg<64, 32, 4, 8, 3, 3>>("64x32_t4x8_s3_3cta", c, false);
-  kahan<SimtCfg<64, 64, 8, 4, 3, 2>>("64x64_t8x4_s3_2cta", c, false);
+  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_t8x8_s3_2cta", c, true);
+  wino_tma<SimtCfg<128, 64, 8, 8, 3, 2>>("tma_128x64_t8x8_s3_2cta", c);
+  wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_t8x8_s4_2cta", c);
+  wino_tma<SimtCfg<64, 64, 8, 8, 4, 4>>("tma_64x64_t8x8_s4_4cta", c);
+  wino_tma<SimtCfg<64, 64, 4, 8, 4, 2>>("tma_64x64_t4x8_s4_2cta", c);
+  wino_tma<SimtCfg<64, 64, 4, 8, 4, 3>>("tma_64x64_t4x8_s4_3cta", c);
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("cpasync_64x64_t4x8_s3_2cta", c, true);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2>>("tma_64x64_t4x8_s3_2cta", c);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 4, 2>>("tma_64x64_t4x8_s4_2cta", c);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 6, 2>>("tma_64x64_t4x8_s6_2cta", c);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 4, 3>>("tma_64x64_t4x8_s4_3cta", c);
+  kahan_tma<SimtCfg<128, 64, 4, 8, 4, 1>>("tma_128x64_t4x8_s4_1cta", c);
   return 0;
 }
