@@ -51,7 +51,11 @@ typedef enum {
   MM_WINOGRAD = 2,         /* P:186-195 WinogradOriginal */
   MM_WINOGRAD_SCALED = 3,  /* P:197-217 WinogradScaled */
   MM_STRASSEN = 4,         /* P:251-291 StrassenNaiv */
-  MM_STRASSEN_WINOGRAD = 5 /* P:294-315 StrassenWinograd */
+  MM_STRASSEN_WINOGRAD = 5, /* P:294-315 StrassenWinograd */
+  /* SURVEY.md 8(f) NEXT-3 fused variants (reading R22) -- not the paper's methods */
+  MM_KAHAN_FUSED = 6,
+  MM_WINOGRAD_FUSED = 7,
+  MM_WINOGRAD_SCALED_FUSED = 8
 } mm_method;
 
 /* Library version string and a human-readable message for a status code. */
@@ -122,7 +126,7 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
 
 /*
  * mm_gemm -- dispatch by mm_method id (levels only used by the Strassen methods,
- * lambda_out only by MM_WINOGRAD_SCALED; both may be 0/NULL otherwise).
+ * lambda_out only by MM_WINOGRAD_SCALED[_FUSED]; both may be 0/NULL otherwise).
  */
 int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
             int32_t levels, void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
@@ -149,6 +153,24 @@ int32_t mm_lambda(double nA, double nB);
 int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                              const double* norms_device, void* workspace, size_t ws_bytes, int32_t* lambda_out,
                              void* stream);
+
+/*
+ * Fused-multiply-add variants (reading R22).  They are NOT the
+ * paper's methods -- the paper's C99 rounds every product separately -- but the same
+ * algorithms with every "s + x*y" contracted into one fma(x, y, s), all orders unchanged:
+ *   mm_kahan_fused           NaivKahan with err = fma(A_ik, B_kj, err)
+ *   mm_winograd_fused        WinogradOriginal with y, z, the pair sums and the odd-P
+ *                            term accumulated by fma
+ *   mm_winograd_scaled_fused WinogradScaled on top of mm_winograd_fused
+ * Each equals the oracle's or_*_fused bit for bit.  Arguments, layout, workspace (the same sizes
+ * as the literal methods: mm_workspace_size(MM_*_FUSED, ...)), stream and error behaviour are
+ * those of mm_kahan / mm_winograd / mm_winograd_scaled.
+ */
+int mm_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream);
+int mm_winograd_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                      void* workspace, size_t ws_bytes, void* stream);
+int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
 
 /*
  * mm_launch_count -- number of kernels this library has launched in this process (a

@@ -31,6 +31,7 @@ BASE_LITERAL = 0
 BASE_FMA = 1
 
 M_STANDARD, M_ON_ARRAY, M_KAHAN, M_UNROLL2, M_UNROLL3, M_UNROLL4, M_FMA, M_WINOGRAD, M_WINOGRAD_SCALED = range(9)
+M_KAHAN_FUSED, M_WINOGRAD_FUSED, M_WINOGRAD_SCALED_FUSED = 9, 10, 11  # NEXT-3 (reading R22)
 
 
 def build(force: bool = False) -> str:
@@ -64,7 +65,7 @@ def lib() -> ctypes.CDLL:
         L.or_norm_inf.argtypes = [dp, i64, i64]
         L.or_norm_inf.restype = d
         for name in ("or_naive_standard", "or_naive_on_array", "or_naive_kahan", "or_naive_fma",
-                     "or_winograd_original"):
+                     "or_winograd_original", "or_naive_kahan_fused", "or_winograd_fused"):
             getattr(L, name).argtypes = [dp, dp, dp, i64, i64, i64]
             getattr(L, name).restype = ctypes.c_int
         L.or_naive_unroll.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64]
@@ -72,6 +73,7 @@ def lib() -> ctypes.CDLL:
         L.or_lambda.argtypes = [d, d]
         L.or_lambda.restype = ctypes.c_int
         L.or_winograd_scaled.argtypes = [dp, dp, dp, i64, i64, i64, ctypes.POINTER(i32)]
+        L.or_winograd_scaled_fused.argtypes = [dp, dp, dp, i64, i64, i64, ctypes.POINTER(i32)]
         L.or_strassen_plan_paper.argtypes = [i64, i64, i64, ctypes.POINTER(i32), ip, ip]
         L.or_strassen_plan_levels.argtypes = [i64, i64, i64, i32, i64, ip, ip, ip]
         L.or_strassen.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, dp, i64, i64, i64, i32, i64, i64, i64]
@@ -168,6 +170,26 @@ def naive_kahan(A, B):
 
 def naive_fma(A, B):
     return _call3("or_naive_fma", A, B)
+
+
+def naive_kahan_fused(A, B):
+    """NEXT-3 (reading R22): NaivKahan with err = fma(A_ik, B_kj, err)."""
+    return _call3("or_naive_kahan_fused", A, B)
+
+
+def winograd_fused(A, B):
+    """NEXT-3 (reading R22): WinogradOriginal with y, z, acc and the odd-P term via fma."""
+    return _call3("or_winograd_fused", A, B)
+
+
+def winograd_scaled_fused(A, B):
+    """NEXT-3: WinogradScaled on top of winograd_fused.  Returns (C, lambda)."""
+    A, B, N, P, M = _ab(A, B)
+    C = np.empty((N, M), dtype=np.float64)
+    lam_out = ctypes.c_int32(0)
+    if lib().or_winograd_scaled_fused(_dp(A), _dp(B), _dp(C), N, P, M, ctypes.byref(lam_out)) != 0:
+        raise ValueError("winograd_scaled_fused failed")
+    return C, int(lam_out.value)
 
 
 def naive_unroll(u: int, A, B):

@@ -469,6 +469,97 @@ int or_int64_gemm(const int64_t* A, const int64_t* B, int64_t* C, int64_t N, int
   return 0;
 }
 
+/* ------------------------------------------------------------------ NEXT-3: fused variants
+ * Not methods of the paper (its C99 rounds every product separately): SURVEY.md 8(f)
+ * NEXT-3 variants in which every "s + x*y" of a method is contracted into ONE C99 fma(x, y, s)
+ * (reading R22 in DESIGN.md); every other operation, and every order, is the method's own. */
+
+/* NaivKahan with x_k = A_ik B_kj folded into the first update: err = fma(A_ik, B_kj, err) */
+static double entry_kahan_fused(const double* A, const double* B, int64_t P, int64_t M, int64_t i, int64_t j) {
+  double t, sum = 0.0, err = 0.0;
+  int64_t k;
+  for (k = 0; k < P; k++) {
+    err = fma(A[IDX(i, k, P)], B[IDX(k, j, M)], err);
+    t = sum + err;
+    err = (sum - t) + err;
+    sum = t;
+  }
+  return sum;
+}
+
+/* P:189 y_i, z_k with y = fma(A[i][2j], A[i][2j+1], y), z = fma(B[2j][k], B[2j+1][k], z) */
+static double winograd_y_fused(const double* A, int64_t P, int64_t i) {
+  double y = 0.0;
+  int64_t j, gamma = P / 2;
+  for (j = 0; j < gamma; j++) y = fma(A[IDX(i, 2 * j, P)], A[IDX(i, 2 * j + 1, P)], y);
+  return y;
+}
+
+static double winograd_z_fused(const double* B, int64_t P, int64_t M, int64_t k) {
+  double z = 0.0;
+  int64_t j, gamma = P / 2;
+  for (j = 0; j < gamma; j++) z = fma(B[IDX(2 * j, k, M)], B[IDX(2 * j + 1, k, M)], z);
+  return z;
+}
+
+/* P:189-192 with acc = fma(A[i][2j] + B[2j+1][k], A[i][2j+1] + B[2j][k], acc) and the odd-P
+ * term c = fma(A[i][P-1], B[P-1][k], c); (acc - y_i) - z_k unchanged */
+static double winograd_entry_yz_fused(const double* A, const double* B, int64_t P, int64_t M, int64_t i, int64_t k,
+                                      double yi, double zk) {
+  double acc = 0.0, c;
+  int64_t j, gamma = P / 2;
+  for (j = 0; j < gamma; j++)
+    acc = fma(A[IDX(i, 2 * j, P)] + B[IDX(2 * j + 1, k, M)], A[IDX(i, 2 * j + 1, P)] + B[IDX(2 * j, k, M)], acc);
+  c = (acc - yi) - zk;
+  if (P % 2 == 1) c = fma(A[IDX(i, P - 1, P)], B[IDX(P - 1, k, M)], c);
+  return c;
+}
+
+int or_naive_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M) {
+  int64_t i, j;
+  if (bad_dims(A, B, C, N, P, M)) return -1;
+  for (i = 0; i < N; i++)
+    for (j = 0; j < M; j++) C[IDX(i, j, M)] = entry_kahan_fused(A, B, P, M, i, j);
+  return 0;
+}
+
+int or_winograd_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M) {
+  int64_t i, k;
+  double *y, *z;
+  if (bad_dims(A, B, C, N, P, M)) return -1;
+  y = (double*)malloc(sizeof(double) * (size_t)N);
+  z = (double*)malloc(sizeof(double) * (size_t)M);
+  if (!y || !z) { free(y); free(z); return -2; }
+  for (i = 0; i < N; i++) y[i] = winograd_y_fused(A, P, i);
+  for (k = 0; k < M; k++) z[k] = winograd_z_fused(B, P, M, k);
+  for (i = 0; i < N; i++)
+    for (k = 0; k < M; k++) C[IDX(i, k, M)] = winograd_entry_yz_fused(A, B, P, M, i, k, y[i], z[k]);
+  free(y);
+  free(z);
+  return 0;
+}
+
+/* WinogradScaled with the fused WinogradOriginal: same lambda, same exact copies */
+int or_winograd_scaled_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             int32_t* lambda_out) {
+  double nA, nB, *As, *Bs;
+  int lambda, rc;
+  if (bad_dims(A, B, C, N, P, M)) return -1;
+  nA = or_norm_inf(A, N, P);
+  nB = or_norm_inf(B, P, M);
+  lambda = or_lambda(nA, nB);
+  As = (double*)malloc(sizeof(double) * (size_t)(N * P));
+  Bs = (double*)malloc(sizeof(double) * (size_t)(P * M));
+  if (!As || !Bs) { free(As); free(Bs); return -2; }
+  or_scalar_mul(ldexp(1.0, lambda), A, As, N, P);
+  or_scalar_mul(ldexp(1.0, -lambda), B, Bs, P, M);
+  rc = or_winograd_fused(As, Bs, C, N, P, M);
+  free(As);
+  free(Bs);
+  if (lambda_out) *lambda_out = lambda;
+  return rc;
+}
+
 /* ------------------------------------------------------------------ per entry */
 double or_entry(int method, const double* A, const double* B, int64_t N, int64_t P, int64_t M,
                 int64_t i, int64_t j, int32_t lambda) {
@@ -487,6 +578,21 @@ double or_entry(int method, const double* A, const double* B, int64_t N, int64_t
     case OR_M_UNROLL4: return entry_unroll(4, A, B, P, M, i, j);
     case OR_M_FMA: return entry_fma(A, B, P, M, i, j);
     case OR_M_WINOGRAD: return winograd_entry_yz(A, B, P, M, i, j, winograd_y(A, P, i), winograd_z(B, P, M, j));
+    case OR_M_KAHAN_FUSED: return entry_kahan_fused(A, B, P, M, i, j);
+    case OR_M_WINOGRAD_FUSED:
+      return winograd_entry_yz_fused(A, B, P, M, i, j, winograd_y_fused(A, P, i), winograd_z_fused(B, P, M, j));
+    case OR_M_WINOGRAD_SCALED_FUSED: {
+      /* row i of 2^lambda A and column j of 2^-lambda B (exact copies, N = 1 and M = 1 views) */
+      double sa = ldexp(1.0, lambda), sb = ldexp(1.0, -lambda), c;
+      int64_t q;
+      double* a = dalloc(P);
+      double* b = dalloc(P);
+      for (q = 0; q < P; q++) { a[q] = sa * A[IDX(i, q, P)]; b[q] = sb * B[IDX(q, j, M)]; }
+      c = winograd_entry_yz_fused(a, b, P, 1, 0, 0, winograd_y_fused(a, P, 0), winograd_z_fused(b, P, 1, 0));
+      free(a);
+      free(b);
+      return c;
+    }
     case OR_M_WINOGRAD_SCALED: {
       /* the row i of 2^lambda A and the column j of 2^-lambda B, then WinogradOriginal's entry */
       double sa = ldexp(1.0, lambda), sb = ldexp(1.0, -lambda), y = 0.0, z = 0.0, acc = 0.0, c;

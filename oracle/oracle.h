@@ -78,6 +78,17 @@ int or_lambda(double nA, double nB);
 int or_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                        int32_t* lambda_out);
 
+/* ---- fused-multiply-add variants (reading R22; NOT the paper's methods,
+ * whose C99 rounds every product separately).  Every "s + x*y" of the method becomes one C99
+ * fma(x, y, s); all other operations and all orders are the method's own. ---- */
+/* NaivKahan with err = fma(A_ik, B_kj, err) */
+int or_naive_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
+/* WinogradOriginal with y, z, acc and the odd-P term accumulated by fma */
+int or_winograd_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
+/* WinogradScaled on top of or_winograd_fused */
+int or_winograd_scaled_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             int32_t* lambda_out);
+
 /* ---- Section 2.4: Strassen ---- */
 #define OR_STRASSEN_NAIV 0     /* P:251-291, 18 block additions per level */
 #define OR_STRASSEN_WINOGRAD 1 /* P:294-315, 15 block additions per level */
@@ -113,6 +124,9 @@ int or_int64_gemm(const int64_t* A, const int64_t* B, int64_t* C, int64_t N, int
 #define OR_M_FMA 6
 #define OR_M_WINOGRAD 7
 #define OR_M_WINOGRAD_SCALED 8 /* uses the lambda argument (global norms needed) */
+#define OR_M_KAHAN_FUSED 9
+#define OR_M_WINOGRAD_FUSED 10
+#define OR_M_WINOGRAD_SCALED_FUSED 11 /* uses the lambda argument */
 double or_entry(int method, const double* A, const double* B, int64_t N, int64_t P, int64_t M,
                 int64_t i, int64_t j, int32_t lambda);
 /* Entry (i,j) of or_strassen(...) computed lazily: only the 2^levels rows of A and

@@ -21,10 +21,11 @@ from . import build as _build
 __all__ = [
     "MMError", "lib", "naive", "naive_on_array", "unroll2", "unroll3", "unroll4", "kahan", "winograd",
     "winograd_scaled", "strassen", "strassen_winograd", "norm_inf", "matmul", "strassen_plan",
-    "workspace_size", "lambda_rule", "METHODS",
+    "workspace_size", "lambda_rule", "METHODS", "kahan_fused", "winograd_fused", "winograd_scaled_fused",
 ]
 
 MM_NAIVE, MM_KAHAN, MM_WINOGRAD, MM_WINOGRAD_SCALED, MM_STRASSEN, MM_STRASSEN_WINOGRAD = range(6)
+MM_KAHAN_FUSED, MM_WINOGRAD_FUSED, MM_WINOGRAD_SCALED_FUSED = 6, 7, 8  # NEXT-3 (R22)
 METHODS = {
     "naive": MM_NAIVE,
     "kahan": MM_KAHAN,
@@ -32,12 +33,16 @@ METHODS = {
     "winograd_scaled": MM_WINOGRAD_SCALED,
     "strassen": MM_STRASSEN,
     "strassen_winograd": MM_STRASSEN_WINOGRAD,
+    "kahan_fused": MM_KAHAN_FUSED,
+    "winograd_fused": MM_WINOGRAD_FUSED,
+    "winograd_scaled_fused": MM_WINOGRAD_SCALED_FUSED,
 }
 
 # every symbol include/mm.h declares
 EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winograd", "mm_winograd_scaled",
            "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
-           "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count")
+           "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
+           "mm_winograd_scaled_fused")
 
 
 class MMError(RuntimeError):
@@ -59,10 +64,12 @@ def lib() -> ctypes.CDLL:
         L.mm_version.restype = ctypes.c_char_p
         L.mm_status_string.restype = ctypes.c_char_p
         L.mm_status_string.argtypes = [ctypes.c_int]
-        for n in ("mm_naive", "mm_kahan"):
+        for n in ("mm_naive", "mm_kahan", "mm_kahan_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp]
-        L.mm_winograd.argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
-        L.mm_winograd_scaled.argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, ctypes.POINTER(i32), vp]
+        for n in ("mm_winograd", "mm_winograd_fused"):
+            getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
+        for n in ("mm_winograd_scaled", "mm_winograd_scaled_fused"):
+            getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, ctypes.POINTER(i32), vp]
         for n in ("mm_strassen", "mm_strassen_winograd"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, i32, vp, sz, vp]
         L.mm_strassen_plan.argtypes = [i64, i64, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i64),
@@ -210,6 +217,24 @@ def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False,
     return (out, int(lam.value)) if return_lambda else out
 
 
+# ---- fused-multiply-add variants (reading R22).  NOT the paper's
+# methods (its C99 rounds every product separately): every "s + x*y" becomes one fma(x, y, s).
+def kahan_fused(A, B, *, out=None, stream=None):
+    """NaivKahan (PAPER.md:122-132) with err = fma(A_ik, B_kj, err)."""
+    return _gemm(MM_KAHAN_FUSED, "mm_kahan_fused", A, B, out, stream=stream)
+
+
+def winograd_fused(A, B, *, out=None, stream=None):
+    """WinogradOriginal with y, z, the pair sums and the odd-P term via fma."""
+    return _gemm(MM_WINOGRAD_FUSED, "mm_winograd_fused", A, B, out, stream=stream)
+
+
+def winograd_scaled_fused(A, B, *, out=None, stream=None, return_lambda: bool = False):
+    """WinogradScaled on top of winograd_fused."""
+    return _gemm(MM_WINOGRAD_SCALED_FUSED, "mm_winograd_scaled_fused", A, B, out, stream=stream,
+                 want_lambda=return_lambda)
+
+
 def launch_count() -> int:
     """Kernels launched by the library so far in this process."""
     return int(lib().mm_launch_count())
@@ -238,13 +263,14 @@ def norm_inf(X: torch.Tensor, *, out=None, stream=None) -> torch.Tensor:
 
 _FUNCS = {
     "naive": naive, "kahan": kahan, "winograd": winograd, "winograd_scaled": winograd_scaled,
-    "strassen": strassen, "strassen_winograd": strassen_winograd,
+    "strassen": strassen, "strassen_winograd": strassen_winograd, "kahan_fused": kahan_fused,
+    "winograd_fused": winograd_fused, "winograd_scaled_fused": winograd_scaled_fused,
 }
 
 
 # methods whose entries depend only on (row of A, column of B): a row block of C is computed
 # bit-identically from the matching row block of A, so host copies can be pipelined by rows
-_ROW_LOCAL = ("naive", "kahan", "winograd")
+_ROW_LOCAL = ("naive", "kahan", "winograd", "kahan_fused", "winograd_fused")
 _STREAMS = {}
 
 

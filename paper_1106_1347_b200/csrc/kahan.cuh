@@ -19,7 +19,8 @@ namespace mmk {
 // 64 x 64 tiles, 128 threads of 4 x 8 outputs, 2 CTAs per SM (tools/tune/simt_tune.cu)
 using KahanDefault = SimtCfg<64, 64, 4, 8, 3, 2>;
 
-template <class CF>
+// FUSED (NEXT-3, reading R22): err = fma(a, b, err) replaces x = a*b; err = err + x
+template <class CF, bool FUSED>
 __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double (&err)[CF::TM][CF::TN],
                                            const double* As, const double* Bs, int kk, int ty, int tx) {
   double a[CF::TM], b[CF::TN];
@@ -35,8 +36,7 @@ __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double
   for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) {
-      const double x = dmul(a[i], b[j]);
-      double e = dadd(err[i][j], x);
+      double e = FUSED ? __fma_rn(a[i], b[j], err[i][j]) : dadd(err[i][j], dmul(a[i], b[j]));
       const double t = dadd(sum[i][j], e);
       e = dadd(dsub(sum[i][j], t), e);
       sum[i][j] = t;
@@ -44,7 +44,7 @@ __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double
     }
 }
 
-template <class CF, int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV, bool FUSED>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     kahan_gemm_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int64_t N,
                       int64_t P, int64_t M) {
@@ -85,10 +85,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     const int64_t k0 = int64_t(kt) * BK;
     if (k0 + BK <= P) {
 #pragma unroll 4
-      for (int kk = 0; kk < BK; ++kk) kahan_step<CF>(sum, err, As, Bs, kk, ty, tx);
+      for (int kk = 0; kk < BK; ++kk) kahan_step<CF, FUSED>(sum, err, As, Bs, kk, ty, tx);
     } else {
       const int kmax = int(P - k0);
-      for (int kk = 0; kk < kmax; ++kk) kahan_step<CF>(sum, err, As, Bs, kk, ty, tx);
+      for (int kk = 0; kk < kmax; ++kk) kahan_step<CF, FUSED>(sum, err, As, Bs, kk, ty, tx);
     }
   }
   cp_async_wait<0>();
@@ -110,10 +110,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   }
 }
 
-template <class CF, int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV, bool FUSED>
 cudaError_t launch_kahan_t(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                            cudaStream_t st) {
-  auto kern = kahan_gemm_kernel<CF, AV, BV, CV>;
+  auto kern = kahan_gemm_kernel<CF, AV, BV, CV, FUSED>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
@@ -126,15 +126,15 @@ cudaError_t launch_kahan_t(const double* A, const double* B, double* C, int64_t 
   return cudaGetLastError();
 }
 
-template <class CF = KahanDefault>
+template <class CF = KahanDefault, bool FUSED = false>
 inline cudaError_t launch_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                                 cudaStream_t st) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
-  if (av && bv && cv) return launch_kahan_t<CF, 2, 2, 2>(A, B, C, N, P, M, st);
-  if (bv && cv) return launch_kahan_t<CF, 1, 2, 2>(A, B, C, N, P, M, st);
-  if (av) return launch_kahan_t<CF, 2, 1, 1>(A, B, C, N, P, M, st);
-  return launch_kahan_t<CF, 1, 1, 1>(A, B, C, N, P, M, st);
+  if (av && bv && cv) return launch_kahan_t<CF, 2, 2, 2, FUSED>(A, B, C, N, P, M, st);
+  if (bv && cv) return launch_kahan_t<CF, 1, 2, 2, FUSED>(A, B, C, N, P, M, st);
+  if (av) return launch_kahan_t<CF, 2, 1, 1, FUSED>(A, B, C, N, P, M, st);
+  return launch_kahan_t<CF, 1, 1, 1, FUSED>(A, B, C, N, P, M, st);
 }
 
 }  // namespace mmk

@@ -34,7 +34,13 @@ constexpr unsigned LN_TILE_BYTES = LN_TILE * sizeof(double);
 constexpr size_t LN_SMEM = 1024 + size_t(LN_STAGES) * LN_TILE * sizeof(double) + LN_STAGES * sizeof(uint64_t);
 static_assert(LN_TK == 32 && LN_LINES == 32, "one lane per tile column / line");
 
-enum { LN_ABS = 0, LN_PAIRS = 1 };
+// LN_PAIRS_FMA: the NEXT-3 fused variant (reading R22), y = fma(x0, x1, y)
+enum { LN_ABS = 0, LN_PAIRS = 1, LN_PAIRS_FMA = 2 };
+
+template <int OP>
+__device__ __forceinline__ double ln_pair(double acc, double x0, double x1) {
+  return OP == LN_PAIRS_FMA ? __fma_rn(x0, x1, acc) : dadd(acc, dmul(x0, x1));
+}
 
 struct LineJob {
   const double* X;               // row-major matrix with leading dimension ld
@@ -194,13 +200,13 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
           for (int q = 0; q < LN_TK / 2; ++q) {
             double2 v = chunk(q);
             if (scaled) v = make_double2(dmul(s, v.x), dmul(s, v.y));
-            acc = dadd(acc, dmul(v.x, v.y));  // y_i += A[i][2j] A[i][2j+1]
+            acc = ln_pair<OP>(acc, v.x, v.y);  // y_i += A[i][2j] A[i][2j+1]
           }
         } else {
           for (int q = 0; q < np; ++q) {
             double2 v = chunk(q);
             if (scaled) v = make_double2(dmul(s, v.x), dmul(s, v.y));
-            acc = dadd(acc, dmul(v.x, v.y));
+            acc = ln_pair<OP>(acc, v.x, v.y);
           }
         }
       }
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
               x0 = dmul(s, x0);
               x1 = dmul(s, x1);
             }
-            acc = dadd(acc, dmul(x0, x1));  // z_k += B[2j][k] B[2j+1][k]
+            acc = ln_pair<OP>(acc, x0, x1);  // z_k += B[2j][k] B[2j+1][k]
           }
         } else {
           for (int j = 0; j < np; ++j) {
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
               x0 = dmul(s, x0);
               x1 = dmul(s, x1);
             }
-            acc = dadd(acc, dmul(x0, x1));
+            acc = ln_pair<OP>(acc, x0, x1);
           }
         }
       }
@@ -329,7 +335,7 @@ inline cudaError_t launch_norms(const double* X0, int64_t r0, int64_t c0, const 
 // As = 2^lambda A, Bs = 2^-lambda B, which are written in the same pass (lambda from norms).
 inline cudaError_t launch_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M,
                              double* As, double* Bs, const unsigned long long* norms, int* lam_out, double* scale_out,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool fused = false) {
   LineLaunch L{};
   L.njobs = 2;
   L.norms = norms;
@@ -350,7 +356,7 @@ inline cudaError_t launch_yz(const double* A, const double* B, double* y, double
     L.job[1].copy = Bs;
     L.job[1].scale_sel = 1;
   }
-  return launch_lines<LN_PAIRS>(L, st);
+  return fused ? launch_lines<LN_PAIRS_FMA>(L, st) : launch_lines<LN_PAIRS>(L, st);
 }
 
 }  // namespace mmk

@@ -114,13 +114,23 @@ int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, 
   return cuda_status(mmk::launch_kahan(A, B, C, N, P, M, S(stream)));
 }
 
+int mm_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  if ((rc = check_device(nullptr))) return rc;
+  return cuda_status(mmk::launch_kahan<mmk::KahanDefault, true>(A, B, C, N, P, M, S(stream)));
+}
+
 size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels) {
   if (N < 1 || P < 1 || M < 1) return 0;
   switch (method) {
     case MM_NAIVE:
-    case MM_KAHAN: return 0;
-    case MM_WINOGRAD: return winograd_ws(N, M);
-    case MM_WINOGRAD_SCALED: return scaled_ws(N, P, M);
+    case MM_KAHAN:
+    case MM_KAHAN_FUSED: return 0;
+    case MM_WINOGRAD:
+    case MM_WINOGRAD_FUSED: return winograd_ws(N, M);
+    case MM_WINOGRAD_SCALED:
+    case MM_WINOGRAD_SCALED_FUSED: return scaled_ws(N, P, M);
     case MM_STRASSEN:
     case MM_STRASSEN_WINOGRAD: {
       mmk::StrassenPlan pl;
@@ -131,8 +141,8 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
   }
 }
 
-int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* workspace,
-                size_t ws_bytes, void* stream) {
+static int winograd_common(bool fused, const double* A, const double* B, double* C, int64_t N, int64_t P,
+                           int64_t M, void* workspace, size_t ws_bytes, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
@@ -141,7 +151,18 @@ int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t 
   if ((rc = check_device(&sms))) return rc;
   double* y = static_cast<double*>(workspace);
   double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N) * 8));
-  return cuda_status(mmk::launch_winograd(A, B, C, y, z, N, P, M, S(stream), sms));
+  return cuda_status(fused ? mmk::launch_winograd<void, true>(A, B, C, y, z, N, P, M, S(stream), sms)
+                           : mmk::launch_winograd<void, false>(A, B, C, y, z, N, P, M, S(stream), sms));
+}
+
+int mm_winograd(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* workspace,
+                size_t ws_bytes, void* stream) {
+  return winograd_common(false, A, B, C, N, P, M, workspace, ws_bytes, stream);
+}
+
+int mm_winograd_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* workspace,
+                      size_t ws_bytes, void* stream) {
+  return winograd_common(true, A, B, C, N, P, M, workspace, ws_bytes, stream);
 }
 
 uint64_t mm_launch_count(void) { return mmk::launch_counter().load(); }
@@ -151,9 +172,9 @@ int mm_winograd_scaled(const double* A, const double* B, double* C, int64_t N, i
   return mm_winograd_scaled_norms(A, B, C, N, P, M, nullptr, workspace, ws_bytes, lambda_out, stream);
 }
 
-int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
-                             const double* norms_device, void* workspace, size_t ws_bytes, int32_t* lambda_out,
-                             void* stream) {
+static int winograd_scaled_common(bool fused, const double* A, const double* B, double* C, int64_t N, int64_t P,
+                                  int64_t M, const double* norms_device, void* workspace, size_t ws_bytes,
+                                  int32_t* lambda_out, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
@@ -172,14 +193,25 @@ int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_
   cudaError_t e = cudaSuccess;
   // K4 norms -> lambda + exact copies 2^lambda A, 2^-lambda B + their y, z -> pair sums.
   // With norms_device the caller's {||A||, ||B||} are used (the same 16 bytes, read as bit patterns).
-  e = mmk::launch_winograd_scaled(A, B, C, N, P, M, norms,
-                                  reinterpret_cast<const unsigned long long*>(norms_device), lam, scale, y, z, As,
-                                  Bs, st, sms);
+  const auto* given = reinterpret_cast<const unsigned long long*>(norms_device);
+  e = fused ? mmk::launch_winograd_scaled<true>(A, B, C, N, P, M, norms, given, lam, scale, y, z, As, Bs, st, sms)
+            : mmk::launch_winograd_scaled<false>(A, B, C, N, P, M, norms, given, lam, scale, y, z, As, Bs, st, sms);
   if (e == cudaSuccess && lambda_out) {
     e = cudaMemcpyAsync(lambda_out, lam, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   return cuda_status(e);
+}
+
+int mm_winograd_scaled_norms(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             const double* norms_device, void* workspace, size_t ws_bytes, int32_t* lambda_out,
+                             void* stream) {
+  return winograd_scaled_common(false, A, B, C, N, P, M, norms_device, workspace, ws_bytes, lambda_out, stream);
+}
+
+int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                             void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream) {
+  return winograd_scaled_common(true, A, B, C, N, P, M, nullptr, workspace, ws_bytes, lambda_out, stream);
 }
 
 int mm_strassen_plan(int64_t N, int64_t P, int64_t M, int32_t levels, int32_t* depth_out, int64_t* Np_out,
@@ -228,6 +260,10 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
     case MM_WINOGRAD_SCALED: return mm_winograd_scaled(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
     case MM_STRASSEN: return mm_strassen(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
     case MM_STRASSEN_WINOGRAD: return mm_strassen_winograd(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+    case MM_KAHAN_FUSED: return mm_kahan_fused(A, B, C, N, P, M, stream);
+    case MM_WINOGRAD_FUSED: return mm_winograd_fused(A, B, C, N, P, M, workspace, ws_bytes, stream);
+    case MM_WINOGRAD_SCALED_FUSED:
+      return mm_winograd_scaled_fused(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
     default: return MM_ERR_ARG;
   }
 }

@@ -84,4 +84,11 @@ __device__ __forceinline__ void simt_tile_coords(int64_t N, int64_t M, int BM, i
   n0 = (in_group / gsize) * BN;
 }
 
+// One Winograd pair: acc + (a0 + b1)(a1 + b0), the product separately rounded (the
+// paper's method) or, FUSED (NEXT-3, reading R22), fma(a0 + b1, a1 + b0, acc).
+template <bool FUSED>
+__device__ __forceinline__ double wino_pair(double acc, double a0, double a1, double b0, double b1) {
+  return FUSED ? __fma_rn(dadd(a0, b1), dadd(a1, b0), acc) : dadd(acc, dmul(dadd(a0, b1), dadd(a1, b0)));
+}
+
 }  // namespace mmk

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
 }
 
 // ---------------------------------------------------------------- K3 Winograd pair sums, TMA-fed (P even)
-template <class CF, int CV>
+template <class CF, int CV, bool FUSED>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(const __grid_constant__ SimtTmaArgs a) {
   using LY = SimtTmaLayout<CF>;
   constexpr int TM = CF::TM, TN = CF::TN;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
+        for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], a0[i], a1[i], b0[j], b1[j]);
     }
     pp.release(s);
   }
@@ -300,7 +300,7 @@ inline cudaError_t launch_kahan_tma(const double* A, const double* B, double* C,
             : launch_simt_tma_t_<kahan_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
 }
 
-template <class CF>
+template <class CF, bool FUSED>
 inline cudaError_t launch_winograd_pairs_tma(const double* A, const double* B, double* C, const double* y,
                                              const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st) {
   using LY = SimtTmaLayout<CF>;
@@ -310,8 +310,8 @@ inline cudaError_t launch_winograd_pairs_tma(const double* A, const double* B, d
   args.z = z;
   const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
   const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
-  return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2>, CF::THREADS, LY::SMEM>(args, grid, st)
-            : launch_simt_tma_t_<winograd_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
+  return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<winograd_tma_kernel<CF, 1, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st);
 }
 
 }  // namespace mmk

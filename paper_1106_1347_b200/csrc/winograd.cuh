@@ -38,7 +38,7 @@ using WinogradTma = SimtCfg<128, 64, 8, 8, 4, 2>;
 // The tiles are loaded with kend = 2*gamma: columns/rows >= 2*gamma are zero-filled, so the
 // odd column never enters acc.  A zero-filled pair adds (0+0)(0+0) = +0 to acc, which leaves
 // acc unchanged (acc starts at +0 and can never become -0), so the last tile needs no guard.
-template <class CF, int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV, bool FUSED>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     winograd_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                     const double* __restrict__ y, const double* __restrict__ z, int64_t N, int64_t P, int64_t M) {
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], dmul(dadd(a0[i], b1[j]), dadd(a1[i], b0[j])));
+        for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], a0[i], a1[i], b0[j], b1[j]);
     }
   }
   cp_async_wait<0>();
@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
         double v = 0.0;
         if (cc < M) {
           v = dsub(dsub(acc[i][2 * c + e], yi), z[cc]);             // (acc - y_i) - z_k
-          if (odd) v = dadd(v, dmul(alast, B[(P - 1) * M + cc]));   // + A_{i,P} B_{P,k}
+          if (odd) v = FUSED ? __fma_rn(alast, B[(P - 1) * M + cc], v)    // + A_{i,P} B_{P,k}
+                             : dadd(v, dmul(alast, B[(P - 1) * M + cc]));
         }
         out[e] = v;
       }
@@ -134,10 +135,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   }
 }
 
-template <class CF, int AV, int BV, int CV>
+template <class CF, int AV, int BV, int CV, bool FUSED>
 cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const double* y, const double* z,
                               int64_t N, int64_t P, int64_t M, cudaStream_t st) {
-  auto kern = winograd_kernel<CF, AV, BV, CV>;
+  auto kern = winograd_kernel<CF, AV, BV, CV, FUSED>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
@@ -151,52 +152,55 @@ cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const
 }
 
 // y, z: device buffers of N and M doubles.
-template <class CF>
+template <class CF, bool FUSED>
 inline cudaError_t launch_winograd_main(const double* A, const double* B, double* C, const double* y,
                                         const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
-  if (av && bv && cv) return launch_winograd_t<CF, 2, 2, 2>(A, B, C, y, z, N, P, M, st);
-  if (bv && cv) return launch_winograd_t<CF, 1, 2, 2>(A, B, C, y, z, N, P, M, st);
-  return launch_winograd_t<CF, 1, 1, 1>(A, B, C, y, z, N, P, M, st);
+  if (av && bv && cv) return launch_winograd_t<CF, 2, 2, 2, FUSED>(A, B, C, y, z, N, P, M, st);
+  if (bv && cv) return launch_winograd_t<CF, 1, 2, 2, FUSED>(A, B, C, y, z, N, P, M, st);
+  return launch_winograd_t<CF, 1, 1, 1, FUSED>(A, B, C, y, z, N, P, M, st);
 }
 
 // the pair-sum kernel with the tile configuration chosen by problem size (y, z already computed)
-template <class CF = void>
+template <class CF = void, bool FUSED = false>
 inline cudaError_t launch_winograd_pairs(const double* A, const double* B, double* C, const double* y,
                                          const double* z, int64_t N, int64_t P, int64_t M, cudaStream_t st,
                                          int sms = 148) {
   if (!std::is_void<CF>::value)
-    return launch_winograd_main<typename std::conditional<std::is_void<CF>::value, WinogradDefault, CF>::type>(
-        A, B, C, y, z, N, P, M, st);
+    return launch_winograd_main<typename std::conditional<std::is_void<CF>::value, WinogradDefault, CF>::type,
+                                FUSED>(A, B, C, y, z, N, P, M, st);
   const int64_t big_tiles = cdiv(N, WinogradDefault::BM) * cdiv(M, WinogradDefault::BN);
   if (big_tiles >= 2 * int64_t(sms)) {
-    if (simt_tma_ok(A, B, N, P, M)) return launch_winograd_pairs_tma<WinogradTma>(A, B, C, y, z, N, P, M, st);
-    return launch_winograd_main<WinogradDefault>(A, B, C, y, z, N, P, M, st);
+    if (simt_tma_ok(A, B, N, P, M))
+      return launch_winograd_pairs_tma<WinogradTma, FUSED>(A, B, C, y, z, N, P, M, st);
+    return launch_winograd_main<WinogradDefault, FUSED>(A, B, C, y, z, N, P, M, st);
   }
-  return launch_winograd_main<WinogradSmall>(A, B, C, y, z, N, P, M, st);
+  return launch_winograd_main<WinogradSmall, FUSED>(A, B, C, y, z, N, P, M, st);
 }
 
-template <class CF = void>
+// WinogradOriginal: y/z pass, then the pair sums.  FUSED: the NEXT-3 variant (reading R22)
+template <class CF = void, bool FUSED = false>
 inline cudaError_t launch_winograd(const double* A, const double* B, double* C, double* y, double* z, int64_t N,
                                    int64_t P, int64_t M, cudaStream_t st, int sms = 148) {
-  cudaError_t e = launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+  cudaError_t e = launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, st, FUSED);
   if (e != cudaSuccess) return e;
-  return launch_winograd_pairs<CF>(A, B, C, y, z, N, P, M, st, sms);
+  return launch_winograd_pairs<CF, FUSED>(A, B, C, y, z, N, P, M, st, sms);
 }
 
 // WinogradScaled: norms (one launch, K4) -> lambda, exact copies 2^lambda A and
 // 2^-lambda B, and their y / z (one fused launch) -> pair sums on the copies.  C is not rescaled
 // (P:216).  Norms are device {||A||, ||B||} bit patterns: given (e.g. the distributed driver's
 // all-reduced ||A||) or, when given == nullptr, computed into `norms`.
+template <bool FUSED = false>
 inline cudaError_t launch_winograd_scaled(const double* A, const double* B, double* C, int64_t N, int64_t P,
                                           int64_t M, unsigned long long* norms, const unsigned long long* given,
                                           int* lam, double* scale, double* y, double* z, double* As, double* Bs,
                                           cudaStream_t st, int sms = 148) {
   cudaError_t e = cudaSuccess;
   if (!given) e = launch_norms(A, N, P, B, P, M, norms, st);
-  if (e == cudaSuccess) e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st);
-  if (e == cudaSuccess) e = launch_winograd_pairs(As, Bs, C, y, z, N, P, M, st, sms);
+  if (e == cudaSuccess) e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st, FUSED);
+  if (e == cudaSuccess) e = launch_winograd_pairs<void, FUSED>(As, Bs, C, y, z, N, P, M, st, sms);
   return e;
 }
 

@@ -14,7 +14,7 @@ import paper_1106_1347_b200 as mm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, nargs=3, default=[8192, 8192, 8192])
-    ap.add_argument("--methods", default="naive,kahan,winograd,winograd_scaled,strassen,strassen_winograd")
+    ap.add_argument("--methods", default="naive,kahan,winograd,winograd_scaled,strassen,strassen_winograd,kahan_fused,winograd_fused")
     ap.add_argument("--levels", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
