@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--levels", type=int, default=2, help="Strassen recursion levels")
     ap.add_argument("--methods", default=",".join(METHODS))
+    ap.add_argument("--panels", type=int, default=8,
+                    help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -206,7 +208,8 @@ def config_dict(args, cfg, world):
         "workload": f"{cfg.key}: A {cfg.N}x{cfg.P}, B {cfg.P}x{cfg.M} float64 ({cfg.dist}), one call of each of "
                     f"{args.methods.replace(',', ', ')} per step",
         "N": cfg.N, "P": cfg.P, "M": cfg.M, "strassen_levels": args.levels,
-        "parallelism": f"row-block dp{world} (B broadcast via NCCL)" if world > 1 else "1 GPU",
+        "parallelism": (f"row-block dp{world} (B broadcast via NCCL; naive: {args.panels} k-panels overlapped)"
+                        if world > 1 else "1 GPU"),
         "l2": "inputs larger than L2 (A, B, C = 537 MB each vs 126 MB L2)" if cfg.N >= 4096
         else "inputs smaller than L2 (not flushed)",
     }
@@ -242,7 +245,7 @@ def run_mine(args):
 
     def one_method(m):
         if world > 1:
-            return mmdist.dist_gemm(m, A, B, out=outs[m], levels=args.levels)
+            return mmdist.dist_gemm(m, A, B, out=outs[m], levels=args.levels, panels=args.panels)
         if m == "winograd_scaled":
             return mm.winograd_scaled(A, B, out=outs[m])
         if m in ("strassen", "strassen_winograd"):
@@ -385,7 +388,7 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M):
                 dA = hA.to(dev, non_blocking=True)
                 if rank == 0:
                     dB.copy_(hB, non_blocking=True)
-                C = mmdist.dist_gemm(m, dA, dB, levels=args.levels)
+                C = mmdist.dist_gemm(m, dA, dB, levels=args.levels, panels=args.panels)
                 hC.copy_(C, non_blocking=True)
                 stream.synchronize()
 

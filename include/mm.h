@@ -70,6 +70,21 @@ const char* mm_status_string(int status);
 int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream);
 
 /*
+ * mm_naive_ex -- the mm_naive kernel on strided operands, optionally accumulating:
+ *   C = A B          (accumulate == 0)
+ *   C = A B + C      (accumulate != 0)   with A N x K (row pitch lda >= K), B K x M (ldb >= M),
+ *                                        C N x M (ldc >= M), all device pointers.
+ * With accumulate the fma chain of every entry STARTS from C's current value and continues over
+ * k = 0..K-1 in order (reading R2), so splitting P into consecutive column panels of A /
+ * row panels of B, in increasing k, reproduces mm_naive bit for bit (up to the sign of zero):
+ *   mm_naive_ex(A, P, B, M, C, M, N, k1, M, 0); mm_naive_ex(A + k1, P, B + k1*M, M, C, M, N, P-k1, M, 1)
+ * -- the building block of the multi-GPU broadcast/compute overlap.
+ * Errors as mm_naive (MM_ERR_ARG also for a pitch smaller than its row); no workspace.
+ */
+int mm_naive_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t N,
+                int64_t K, int64_t M, int32_t accumulate, void* stream);
+
+/*
  * mm_kahan -- NaivKahan: each entry is the compensated sum of the products
  * A_ik B_kj, k increasing, with the update of P:122-132
  * (err = err + x; t = sum + err; err = (sum - t) + err; sum = t), result `sum`.

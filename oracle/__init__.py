@@ -69,6 +69,7 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).argtypes = [dp, dp, dp, i64, i64, i64]
             getattr(L, name).restype = ctypes.c_int
         L.or_naive_unroll.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64]
+        L.or_naive_fma_acc.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, i64]
         L.or_winograd_yz.argtypes = [dp, dp, dp, dp, i64, i64, i64]
         L.or_lambda.argtypes = [d, d]
         L.or_lambda.restype = ctypes.c_int
@@ -170,6 +171,24 @@ def naive_kahan(A, B):
 
 def naive_fma(A, B):
     return _call3("or_naive_fma", A, B)
+
+
+def naive_fma_acc(A, B, C):
+    """C (float64 ndarray, modified in place and returned) = A B + C, continuing each entry's
+    fma chain from C (reading R2; the panel step of SURVEY 8(f) NEXT-4).  A, B may be 2-D
+    row-major views (unit column stride)."""
+    for X in (A, B, C):
+        if X.dtype != np.float64 or X.ndim != 2 or X.strides[1] != 8:
+            raise ValueError("row-major float64 matrices with unit column stride required")
+    N, K = A.shape
+    M = B.shape[1]
+    if B.shape[0] != K or C.shape != (N, M):
+        raise ValueError("shape mismatch")
+    rc = lib().or_naive_fma_acc(_dp(A), A.strides[0] // 8, _dp(B), B.strides[0] // 8, _dp(C), C.strides[0] // 8,
+                                N, K, M)
+    if rc != 0:
+        raise ValueError("or_naive_fma_acc failed")
+    return C
 
 
 def naive_kahan_fused(A, B):

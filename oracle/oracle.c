@@ -171,6 +171,22 @@ int or_naive_fma(const double* A, const double* B, double* C, int64_t N, int64_t
   return 0;
 }
 
+/* Reading R2 continued: the chain of or_naive_fma started from C's current value,
+ * C_ij = fma(A_i,K-1 B_K-1,j, ... fma(A_i0 B_0j, C_ij)), strided operands.  Consecutive k-panels
+ * therefore compose to or_naive_fma (SURVEY 8(f) NEXT-4's panelised product). */
+int or_naive_fma_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                     int64_t N, int64_t K, int64_t M) {
+  int64_t i, j, k;
+  if (!A || !B || !C || N < 1 || K < 1 || M < 1 || lda < K || ldb < M || ldc < M) return -1;
+  for (i = 0; i < N; i++)
+    for (j = 0; j < M; j++) {
+      double aux = C[i * ldc + j];
+      for (k = 0; k < K; k++) aux = fma(A[i * lda + k], B[k * ldb + j], aux);
+      C[i * ldc + j] = aux;
+    }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ Section 2.3 */
 static double winograd_y(const double* A, int64_t P, int64_t i) {
   double y = 0.0;

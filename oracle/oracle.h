@@ -63,6 +63,11 @@ int or_naive_unroll(int u, const double* A, const double* B, double* C, int64_t 
  * k increasing.  This is what one FP64 tensor-core DMMA chain computes (probe P3). */
 int or_naive_fma(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
 
+/* Reading R2 continued: C = A B + C where every entry's fma chain starts
+ * from C's current value; A N x K (pitch lda), B K x M (pitch ldb), C N x M (pitch ldc). */
+int or_naive_fma_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                     int64_t N, int64_t K, int64_t M);
+
 /* ---- Section 2.3: Winograd ---- */
 /* gamma = floor(P/2); y_i = sum_{j<gamma} A[i][2j]*A[i][2j+1];
  * z_k = sum_{j<gamma} B[2j][k]*B[2j+1][k]  (0-based form of A_{i,2j-1}A_{i,2j}) */

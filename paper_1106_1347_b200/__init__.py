@@ -42,7 +42,7 @@ METHODS = {
 EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winograd", "mm_winograd_scaled",
            "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
            "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
-           "mm_winograd_scaled_fused")
+           "mm_winograd_scaled_fused", "mm_naive_ex")
 
 
 class MMError(RuntimeError):
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
         L.mm_status_string.argtypes = [ctypes.c_int]
         for n in ("mm_naive", "mm_kahan", "mm_kahan_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp]
+        L.mm_naive_ex.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, i64, i32, vp]
         for n in ("mm_winograd", "mm_winograd_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
         for n in ("mm_winograd_scaled", "mm_winograd_scaled_fused"):
@@ -176,6 +177,23 @@ def _gemm(method: int, name: str, A, B, out=None, levels: int = 0, stream=None, 
 def naive(A, B, *, out=None, stream=None):
     """NaivStandard on the FP64 tensor cores."""
     return _gemm(MM_NAIVE, "mm_naive", A, B, out, stream=stream)
+
+
+def naive_panel(A, B, C, *, accumulate: bool, stream=None):
+    """C = A B (+ C) on strided 2-D views (mm_naive_ex): with accumulate=True each entry's fma
+    chain continues from C, so consecutive k-panels reproduce naive() bit for bit.  A, B, C must
+    be float64 CUDA tensors with unit column stride (row-major views, e.g. A[:, k0:k1])."""
+    for t in (A, B, C):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.dim() == 2
+                and t.stride(1) == 1):
+            raise ValueError("A, B, C must be row-major float64 CUDA matrices (unit column stride)")
+    N, K = A.shape
+    if B.shape[0] != K or C.shape != (N, B.shape[1]):
+        raise ValueError(f"shape mismatch: {tuple(A.shape)} x {tuple(B.shape)} -> {tuple(C.shape)}")
+    M = B.shape[1]
+    _check(lib().mm_naive_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), N, K,
+                             M, 1 if accumulate else 0, _stream_handle(stream, A.device)), "mm_naive_ex")
+    return C
 
 
 # NaivOnArray and the unrolled variants compute the same product; on the GPU they are the

@@ -29,6 +29,7 @@ struct GemmProblem {
   int64_t lda, ldb, ldc;  // leading dimensions (elements)
   int64_t sA, sB, sC;     // batch strides (elements)
   int64_t batch;
+  int accumulate = 0;     // 1: every entry's fma chain starts from C's current value (C = A B + C)
 };
 
 template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1, int BK_ = 16>
@@ -130,6 +131,19 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_dmma_kernel
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (pr.accumulate) {  // continue each entry's chain from C (same mapping as the epilogue)
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int64_t row = m0 + wm * CF::WTM + g + 8 * mi;
+      if (row >= pr.N) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) {
+        const int64_t col = n0 + wn * CF::WTN + 8 * nj + 2 * t;
+        if (col < pr.M) acc[mi][nj][0] = C[row * pr.ldc + col];
+        if (col + 1 < pr.M) acc[mi][nj][1] = C[row * pr.ldc + col + 1];
+      }
+    }
+  }
 
   const int KT = int(cdiv(pr.P, BK));
 #pragma unroll

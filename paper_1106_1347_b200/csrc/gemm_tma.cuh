@@ -10,8 +10,9 @@
 //    Ragged edges are zero-filled by the TMA unit.
 //  * One thread issues the copies; completion is counted in bytes on a per-stage "full"
 //    mbarrier, and each warp releases a stage on its "empty" mbarrier -- no CTA-wide barrier
-//    in the main loop.  The refill of the stage of tile kt-1 is issued at the top of tile kt,
-//    so STAGES-1 tiles are in flight while a tile is multiplied.
+//    in the main loop.  Tile kt-1's stage is released and refilled at the top of tile kt (after
+//    the loop back edge, so every LDS of it has completed), so STAGES-1 tiles are in flight
+//    while a tile is multiplied.
 //  * Bank-conflict-free fragment loads under the TMA swizzle come from permuting which tile
 //    rows / columns a fragment's lanes own (the 8x8 fragment rows g -> rho(g) =
 //    0,2,4,6,1,3,5,7 and columns g -> sigma(g) = 0,1,8,9,2,3,10,11 (+4 for the second fragment
@@ -107,19 +108,40 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
 
   // fragment addressing (doubles): A row of fragment mi = wm*WTM + 8 mi + rho(g)
   const int rho = rho8(g);
+  if (pr.accumulate) {  // continue each entry's chain from C (same mapping as the epilogue)
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int64_t row = int64_t(m0) + wm * CF::WTM + 8 * mi + rho;
+      if (row >= pr.N) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) {
+        const int64_t col = int64_t(n0) + wn * CF::WTN + 16 * (nj >> 1) + sigma8(2 * t) + 4 * (nj & 1);
+        if (col < pr.M) acc[mi][nj][0] = C[row * pr.ldc + col];
+        if (col + 1 < pr.M) acc[mi][nj][1] = C[row * pr.ldc + col + 1];
+      }
+    }
+  }
   const int a_base = (wm * CF::WTM + rho) * 16;
   const int sig0 = sigma8(g), sig1 = sig0 + 4;
   const int b_box0 = (wn * CF::WTN) / 16;
 
 #pragma unroll 1
   for (int kt = 0; kt < KT; ++kt) {
-    if (tid == 0 && kt >= 1) {  // refill the stage of tile kt-1 once every warp has released it
+    if (kt >= 1) {
+      // Release tile kt-1's stage HERE, after the loop back edge: every DMMA of tile kt-1 has been
+      // issued, so every LDS feeding it has returned its data (operand scoreboards).  Releasing at
+      // the end of iteration kt-1 instead lets ptxas hoist the arrive above DMMAs whose LDS are
+      // still in flight, and the TMA refill can then overwrite the stage under them (a
+      // write-after-read race, observed as sporadic wrong 32x32 blocks).
+      const int sp = (kt - 1) % STAGES;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + sp);
       const int kp = kt - 1 + STAGES;
-      if (kp < KT) {
-        const int sp = (kt - 1) % STAGES;
+      if (tid == 0 && kp < KT) {  // refill it once every warp has released it
         mbar_wait(empty + sp, unsigned(((kt - 1) / STAGES) & 1));
         issue(kp, sp);
       }
+      __syncwarp();
     }
     const int s = kt % STAGES;
     mbar_wait(full + s, unsigned((kt / STAGES) & 1));
@@ -143,8 +165,6 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
 #pragma unroll
         for (int nj = 0; nj < NJ; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
   }
 
   // epilogue: fragment (mi, nj) holds C[row][col], C[row][col + 1] with

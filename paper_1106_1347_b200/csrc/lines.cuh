@@ -169,6 +169,19 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   double acc = 0.0;
 #pragma unroll 1
   for (int64_t kt = 0; kt < KT; ++kt) {
+    if (kt >= 1) {
+      // refill tile kt-1's stage with tile kt-1+STAGES here, after the loop back edge: every op
+      // consuming its shared-memory loads has issued, so those loads have completed (refilling
+      // at the end of iteration kt-1 would let ptxas hoist the copy above in-flight loads)
+      const int64_t nk = kt - 1 + LN_STAGES;
+      if (jb.bulk) fence_proxy_async_smem();
+      __syncwarp();
+      if (nk < KT) {
+        const int sp = int((kt - 1) % LN_STAGES);
+        ln_issue(L, ji, ln_smem + sp * LN_TILE, bars + sp, l0, nk, lane);
+      }
+      __syncwarp();
+    }
     const int st = int(kt % LN_STAGES);
     mbar_wait(bars + st, unsigned((kt / LN_STAGES) & 1));
     const double* t = ln_smem + st * LN_TILE;
@@ -247,14 +260,6 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
         if (lane < lv)
           for (int k = 0; k < kv; ++k) jb.copy[(k0 + k) * jb.ld + l0 + lane] = dmul(s, t[k * LN_LINES + lane]);
-      }
-    }
-    __syncwarp();  // every lane is done with stage st before it is refilled with tile kt + STAGES
-    {
-      const int64_t nk = kt + LN_STAGES;
-      if (nk < KT) {
-        if (jb.bulk) fence_proxy_async_smem();
-        ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, nk, lane);
       }
     }
   }

@@ -107,6 +107,19 @@ int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, 
   return cuda_status(mmk::launch_dgemm(pr, S(stream), sms));
 }
 
+int mm_naive_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t N,
+                int64_t K, int64_t M, int32_t accumulate, void* stream) {
+  if (!A || !B || !C || N < 1 || K < 1 || M < 1 || lda < K || ldb < M || ldc < M) return MM_ERR_ARG;
+  if (!mul_ok(N, lda) || !mul_ok(K, ldb) || !mul_ok(N, ldc)) return MM_ERR_ARG;
+  const int64_t na = (N - 1) * lda + K, nb = (K - 1) * ldb + M, nc = (N - 1) * ldc + M;  // spans
+  if (overlaps(C, nc, A, na) || overlaps(C, nc, B, nb)) return MM_ERR_ALIAS;
+  int sms = 148, rc;
+  if ((rc = check_device(&sms))) return rc;
+  mmk::GemmProblem pr{A, B, C, N, K, M, lda, ldb, ldc, 0, 0, 0, 1};
+  pr.accumulate = accumulate ? 1 : 0;
+  return cuda_status(mmk::launch_dgemm(pr, S(stream), sms));
+}
+
 int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;

@@ -12,7 +12,8 @@
 //    ty + TYM i of A (4 consecutive rows per warp -> 4 distinct chunks, broadcast over tx) and
 //    the column pairs 2 tx + 16 c of B (box c, chunk tx -> 8 distinct chunks): conflict free.
 //  * One thread issues the copies into a STAGES-deep ring with per-stage full (expect_tx) and
-//    empty (one arrival per warp) mbarriers: no CTA-wide barrier in the main loop.
+//    empty (one arrival per warp) mbarriers: no CTA-wide barrier in the main loop; a stage is
+//    released at the top of the next tile (after every read of it has completed).
 //  * TMA zero-fills out-of-range rows/columns; the Kahan k-loop still stops exactly at P (a
 //    zero term is not a no-op for the compensated update) and Winograd's pair loop ends at
 //    gamma = P/2 (P is even on this path).
@@ -87,23 +88,24 @@ struct SimtPipe {
     if (threadIdx.x == 0)
       for (int s = 0; s < CF::STAGES && s < KT; ++s) issue(a, s, s);
   }
-  // top of tile kt: refill the stage of tile kt-1, then wait for tile kt; returns its stage
+  // top of tile kt: release tile kt-1's stage (after the loop back edge every FP64 op reading
+  // its LDS results has issued, so the loads have completed -- see gemm_tma.cuh), refill it
+  // once every warp released it, then wait for tile kt; returns its stage
   __device__ __forceinline__ int acquire(const SimtTmaArgs& a, int kt) {
-    if (threadIdx.x == 0 && kt >= 1) {
+    if (kt >= 1) {
+      const int sp = (kt - 1) % CF::STAGES;
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + sp);
       const int kp = kt - 1 + CF::STAGES;
-      if (kp < KT) {
-        const int sp = (kt - 1) % CF::STAGES;
+      if (threadIdx.x == 0 && kp < KT) {
         mbar_wait(empty + sp, unsigned(((kt - 1) / CF::STAGES) & 1));
         issue(a, kp, sp);
       }
+      __syncwarp();  // reconverge warp 0 before the tile's math (else lanes 1-31 run it apart)
     }
     const int s = kt % CF::STAGES;
     mbar_wait(full + s, unsigned((kt / CF::STAGES) & 1));
     return s;
-  }
-  __device__ __forceinline__ void release(int s) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
   }
 };
 
@@ -161,7 +163,6 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
       const int kmax = int(a.P - k0);  // stop exactly at P
       for (int kk = 0; kk < kmax; ++kk) step(As, Bs, kk);
     }
-    pp.release(s);
   }
 
 #pragma unroll
@@ -230,7 +231,6 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], a0[i], a1[i], b0[j], b1[j]);
     }
-    pp.release(s);
   }
 
 #pragma unroll

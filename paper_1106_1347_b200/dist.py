@@ -11,8 +11,16 @@ no split-K and y_i / z_k are per row / column -- so the classical, Kahan, Winogr
 Winograd shards are bitwise equal to the corresponding rows of the 1-GPU product.  Strassen on
 a shard recurses on (N_local x P x M) and agrees within its tolerance only.
 
+Broadcast/compute overlap, NaivStandard only: with panels > 1, B is
+broadcast as `panels` consecutive row panels (contiguous in memory), all enqueued at once on
+NCCL's stream; the product is accumulated panel by panel with mm_naive_ex(accumulate=1), each
+launch waiting (on the device, not the host) for its own panel only, so the transfer of panel
+i+1 overlaps the DMMA work on panel i.  Because every entry's fma chain continues from C in k
+order (reading R2), the result is bitwise the one-shot product at any panel count.
+
 The compute and norm callables are injectable so that the host-side logic (sharding, the
-broadcast, the max-reduction and lambda) is testable with world_size 2 on CPU (gloo).
+broadcast, the max-reduction and lambda, the panel schedule) is testable with world_size 2 on
+CPU (gloo).
 """
 from __future__ import annotations
 
@@ -44,14 +52,45 @@ def _default_norm(X):
     return mm.norm_inf(X)
 
 
+def _default_panel(A_panel, B_panel, out, accumulate: bool):
+    import paper_1106_1347_b200 as mm
+
+    return mm.naive_panel(A_panel, B_panel, out, accumulate=accumulate)
+
+
+def panel_bounds(P: int, panels: int):
+    """Consecutive k-panels [k0, k1) covering 0..P, boundaries even (16-byte aligned views)."""
+    panels = max(1, min(panels, P))
+    cuts = sorted({min(P, 2 * ((P * i) // (2 * panels))) for i in range(1, panels)} - {0, P})
+    b = [0] + cuts + [P]
+    return list(zip(b[:-1], b[1:]))
+
+
+def _dist_naive_panels(A_local, B, out, root, group, panels, panel_compute):
+    P, M = B.shape
+    bounds = panel_bounds(P, panels)
+    works = [dist.broadcast(B[k0:k1], src=root, group=group, async_op=True) for k0, k1 in bounds]
+    if out is None:
+        out = torch.empty((A_local.shape[0], M), dtype=B.dtype, device=B.device)
+    for i, (k0, k1) in enumerate(bounds):
+        works[i].wait()  # NCCL: the current stream waits for this panel only; gloo: the host waits
+        if A_local.shape[0] > 0:
+            panel_compute(A_local[:, k0:k1], B[k0:k1], out, i > 0)
+    return out
+
+
 def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None,
               root: int = 0, group=None, levels: int = 2, compute: Optional[Callable] = None,
-              norm: Optional[Callable] = None) -> torch.Tensor:
+              norm: Optional[Callable] = None, panels: int = 1,
+              panel_compute: Optional[Callable] = None) -> torch.Tensor:
     """C_local = A_local B on every rank.  B must be allocated (P x M) on every rank; its content
-    on `root` is broadcast (in place) before the product.  A rank with no rows still takes part
-    in the collectives and returns an empty (0 x M) result."""
+    on `root` is broadcast (in place) before / during the product.  A rank with no rows still
+    takes part in the collectives and returns an empty (0 x M) result.  panels > 1 (method
+    "naive" only): panelised broadcast overlapped with the accumulation (NEXT-4)."""
     compute = compute or _default_compute
     norm = norm or _default_norm
+    if method == "naive" and panels > 1:
+        return _dist_naive_panels(A_local, B, out, root, group, panels, panel_compute or _default_panel)
     dist.broadcast(B, src=root, group=group)
     norms = None
     if method == "winograd_scaled":

@@ -41,6 +41,16 @@ def _oracle_compute(method, A, B, out, levels, norms):
     return torch.from_numpy(C)
 
 
+def _oracle_panel(A_panel, B_panel, out, accumulate):
+    import oracle
+
+    C = out.numpy()
+    if not accumulate:
+        C[...] = 0.0
+    oracle.naive_fma_acc(A_panel.numpy(), B_panel.numpy(), C)
+    return out
+
+
 def _oracle_norm(X):
     import oracle
 
@@ -69,9 +79,27 @@ def _worker(rank, world, port, N, P, M, seed, q):
             C = dist_gemm(m, A_loc, Bt, compute=_oracle_compute, norm=_oracle_norm)
             out[m] = C.numpy().copy()
         assert np.array_equal(Bt.numpy(), B)  # broadcast delivered B everywhere
+        # NEXT-4: panelised broadcast + chain-continuing accumulation, B re-broadcast from scratch
+        for panels in (2, 3, 5):
+            Bp = torch.from_numpy(B.copy()) if rank == 0 else torch.full((P, M), np.nan, dtype=torch.float64)
+            C = dist_gemm("naive", A_loc, Bp, panels=panels, panel_compute=_oracle_panel)
+            assert np.array_equal(Bp.numpy(), B)
+            out[f"naive_p{panels}"] = C.numpy().copy()
         q.put((rank, lo, hi, out))
     finally:
         dist.destroy_process_group()
+
+
+def test_panel_bounds():
+    from paper_1106_1347_b200.dist import panel_bounds
+
+    for P in (1, 2, 7, 16, 1001, 8192):
+        for n in (1, 2, 3, 8, 64):
+            b = panel_bounds(P, n)
+            assert b[0][0] == 0 and b[-1][1] == P
+            assert all(k0 < k1 for k0, k1 in b) and all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+            assert all(k0 % 2 == 0 for k0, _ in b)
+            assert len(b) <= n
 
 
 def _run(world, N, P, M, seed):
@@ -107,5 +135,5 @@ def test_row_sharded_bitwise(shape):
     for rank, lo, hi, out in res:
         for m, C in out.items():
             assert C.shape == (hi - lo, M)
-            assert np.array_equal(C, full[m][lo:hi]), (rank, m)
+            assert np.array_equal(C, full[m.split("_p")[0]][lo:hi]), (rank, m)
     assert sum(hi - lo for _, lo, hi, _ in res) == N

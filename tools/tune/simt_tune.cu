@@ -86,7 +86,7 @@ template <class CF>
 void wino_tma(const char* name, Ctx& c) {
   timeit("winograd", name, CF::THREADS, SimtTmaLayout<CF>::SMEM, c, c.R, [&] {
     launch_yz(c.A, c.B, c.y, c.z, c.n, c.n, c.n, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
-    launch_winograd_pairs_tma<CF>(c.A, c.B, c.C, c.y, c.z, c.n, c.n, c.n, 0);
+    launch_winograd_pairs_tma<CF, false>(c.A, c.B, c.C, c.y, c.z, c.n, c.n, c.n, 0);
   }, 2.0);
 }
 int main(int argc, char** argv) {
