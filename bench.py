@@ -326,7 +326,8 @@ def run_mine(args):
     kernels = {
         "naive": ("tensor", 2.0 * n_eff * P * M, peaks["dmma_tflops"], "dgemm_tma_kernel"),
         "kahan": ("alu", 5.0 * n_eff * P * M, peaks["simt_op_tflops"], "kahan_gemm_kernel"),
-        "winograd": ("alu", 4.0 * n_eff * M * (P // 2), peaks["simt_op_tflops"], "winograd_kernel"),
+        "winograd": ("alu", 4.0 * n_eff * M * (P // 2), peaks["simt_op_tflops"],
+                     "winograd_tma_kernel" if P % 2 == 0 and M % 2 == 0 else "winograd_kernel"),
     }
     roof_all = {}
     for m, (bound, fl, pk, kname) in kernels.items():
