@@ -22,6 +22,7 @@ __all__ = [
     "MMError", "lib", "naive", "naive_on_array", "unroll2", "unroll3", "unroll4", "kahan", "winograd",
     "winograd_scaled", "strassen", "strassen_winograd", "norm_inf", "matmul", "strassen_plan",
     "workspace_size", "lambda_rule", "METHODS", "kahan_fused", "winograd_fused", "winograd_scaled_fused",
+    "naive_panel", "matmul_methods",
 ]
 
 MM_NAIVE, MM_KAHAN, MM_WINOGRAD, MM_WINOGRAD_SCALED, MM_STRASSEN, MM_STRASSEN_WINOGRAD = range(6)
@@ -351,3 +352,71 @@ def matmul(A: torch.Tensor, B: torch.Tensor, method: str = "naive", *, levels: i
     s_out.synchronize()
     s.synchronize()
     return out
+
+
+def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2, device=None,
+                   outs: Optional[dict] = None, row_blocks: int = 4) -> dict:
+    """The shape of the paper's test program: several methods applied to the
+    SAME host operands.  A and B (pinned host float64) are copied to the device once; every
+    method's product is copied back into outs[method] (pinned host, allocated if missing) on a
+    copy stream while the next method computes.  When the first method is row-local its row
+    blocks start as soon as their rows of A have landed; when the last one is, its result
+    streams back by row blocks.  Each product is bitwise the one-shot device call's."""
+    methods = list(methods)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    s = torch.cuda.current_stream(dev)
+    s_in, s_out = _aux_streams(dev)
+    N, P = A.shape
+    M = B.shape[1]
+    outs = {} if outs is None else outs
+    for m in methods:
+        if m not in outs:
+            outs[m] = torch.empty((N, M), dtype=torch.float64, pin_memory=True)
+    rb = max(1, min(row_blocks, N // 2)) if N >= 2 else 1
+    bounds = [(N * b) // rb for b in range(rb + 1)]
+    s_in.wait_stream(s)
+    with torch.cuda.stream(s_in):
+        dB = B.to(dev, non_blocking=True)
+        dA = torch.empty((N, P), dtype=torch.float64, device=dev)
+        a_ready = []
+        for b in range(rb):
+            lo, hi = bounds[b], bounds[b + 1]
+            dA[lo:hi].copy_(A[lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+            a_ready.append(ev)
+    bufs = [torch.empty((N, M), dtype=torch.float64, device=dev) for _ in range(min(2, len(methods)))]
+    buf_free = [None] * len(bufs)
+    for i, m in enumerate(methods):
+        f = _FUNCS[m]
+        kw = {"levels": levels} if m in ("strassen", "strassen_winograd") else {}
+        k = i % len(bufs)
+        if buf_free[k] is not None:
+            s.wait_event(buf_free[k])  # the D2H of the product that last used this buffer is done
+        buf = bufs[k]
+        row_local = m in _ROW_LOCAL and rb > 1
+        first, last = i == 0, i == len(methods) - 1
+        if row_local and (first or last):
+            for b in range(rb):
+                lo, hi = bounds[b], bounds[b + 1]
+                s.wait_event(a_ready[b])
+                f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
+                s_out.wait_stream(s)
+                with torch.cuda.stream(s_out):
+                    outs[m][lo:hi].copy_(buf[lo:hi], non_blocking=True)
+        else:
+            s.wait_event(a_ready[-1])
+            f(dA, dB, out=buf, stream=s, **kw)
+            s_out.wait_stream(s)
+            with torch.cuda.stream(s_out):
+                outs[m].copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s_out)
+        buf_free[k] = ev
+    for t in [dA, dB] + bufs:
+        t.record_stream(s_in)
+        t.record_stream(s)
+        t.record_stream(s_out)
+    s_out.synchronize()
+    s.synchronize()
+    return outs

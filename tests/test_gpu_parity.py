@@ -378,3 +378,17 @@ def test_norm_inf_many_shapes():
         for cols in (1, 2, 31, 32, 33, 64, 65, 130):
             X = workload.custom(rows, cols, 1, rows * 1000 + cols)[0] * 7.0
             assert mm.norm_inf(dev(X)).item() == oracle.norm_inf(X), (rows, cols)
+
+
+def test_matmul_methods_bitwise():
+    """matmul_methods (the paper's test-program shape: every method on the same host operands,
+    copies overlapped with the kernels) gives every method's one-shot device result bit for bit."""
+    A, B = workload.custom(517, 130, 258, seed=12)
+    hA = torch.from_numpy(A).pin_memory()
+    hB = torch.from_numpy(B).pin_memory()
+    order = ["naive", "strassen", "winograd_scaled", "winograd", "kahan"]
+    outs = mm.matmul_methods(hA, hB, order, levels=1)
+    dA, dB = dev(A), dev(B)
+    for m in order:
+        ref = host(run(m, dA, dB, 1))
+        assert np.array_equal(outs[m].numpy(), ref), m
