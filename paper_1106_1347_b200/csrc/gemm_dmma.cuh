@@ -32,7 +32,8 @@ struct GemmProblem {
   int accumulate = 0;     // 1: every entry's fma chain starts from C's current value (C = A B + C)
 };
 
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1, int BK_ = 16>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MIN_BLOCKS_ = 1, int BK_ = 16,
+          int GROUP_M_ = 8>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_, MIN_BLOCKS = MIN_BLOCKS_;
@@ -40,7 +41,7 @@ struct GemmCfg {
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   static constexpr int MI = WTM / 8, NJ = WTN / 8;
   static constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
-  static constexpr int GROUP_M = 8;
+  static constexpr int GROUP_M = GROUP_M_;  // tile rows per rasterisation group (L2 reuse)
   static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
   static_assert((A_ELEMS / 2) % THREADS == 0 && (B_ELEMS / 2) % THREADS == 0, "loader split");

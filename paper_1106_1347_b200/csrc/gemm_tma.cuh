@@ -243,10 +243,13 @@ inline cudaError_t launch_dgemm_tma(const GemmProblem& pr, cudaStream_t st) {
             : launch_tma_t<dgemm_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
 }
 
+#ifndef GEMM_TMA_GROUP_M
+#define GEMM_TMA_GROUP_M 8
+#endif
 // the production configuration of the TMA path: 64 x 64 tiles, 4 warps of 32 x 32, 4 stages,
 // 3 CTAs (12 warps) per SM -- 36.1 TF at 8192^3, 34.0 at 2048^3, 27.5 at 1024^3 on B200
 // (tools/tune/gemm_tune.cu, profiles/r01/gemm_tune_tma.jsonl; cuBLAS DGEMM: 35.5 at 8192^3)
-using GemmTma = GemmCfg<64, 64, 2, 2, 4, 3>;
+using GemmTma = GemmCfg<64, 64, 2, 2, 4, 3, 16, GEMM_TMA_GROUP_M>;
 
 // K1 entry: TMA-staged kernel when the operands allow a tensor map, else the cp.async kernel
 // (same k order, bitwise the same result)

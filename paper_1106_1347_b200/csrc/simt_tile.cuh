@@ -73,7 +73,10 @@ __device__ __forceinline__ int simt_row(int ty, int i) {
 
 // Grouped rasterisation of a 1-D grid of BM x BN tiles (8 tile rows per group) for L2 reuse.
 __device__ __forceinline__ void simt_tile_coords(int64_t N, int64_t M, int BM, int BN, int64_t& m0, int64_t& n0) {
-  constexpr int GROUP = 8;
+#ifndef SIMT_GROUP_M
+#define SIMT_GROUP_M 8
+#endif
+  constexpr int GROUP = SIMT_GROUP_M;
   const int64_t tiles_m = cdiv(N, BM), tiles_n = cdiv(M, BN);
   const int64_t tile = blockIdx.x;
   const int64_t group = tile / (GROUP * tiles_n);

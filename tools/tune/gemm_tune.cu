@@ -70,13 +70,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
-  run<GemmCfg<128, 64, 2, 2, 4, 2>>("cpasync_128x64_w2x2_s4_2cta", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 3, 4>, true>("tma_64x64_w2x2_s3_4cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 2, 6>, true>("tma_64x64_w2x2_s2_6cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 128, 2, 2, 3, 3>, true>("tma_64x128_w2x2_s3_3cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<128, 64, 4, 2, 4, 2>, true>("tma_128x64_w4x2_s4_2cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<128, 64, 4, 2, 3, 3>, true>("tma_128x64_w4x2_s3_3cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta_again", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 8>, true>("tma_64x64_s4_3cta_g8", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 4>, true>("tma_64x64_s4_3cta_g4", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 16>, true>("tma_64x64_s4_3cta_g16", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 21>, true>("tma_64x64_s4_3cta_g21", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 32>, true>("tma_64x64_s4_3cta_g32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 8>, true>("tma_64x64_s4_3cta_g8_again", A, B, C, R, n, reps, bad);
   return 0;
 }
