@@ -197,18 +197,6 @@ inline bool gemm_tma_ok(const GemmProblem& pr) {
   return true;
 }
 
-inline bool encode_3d(CUtensorMap* map, const double* X, int64_t rows, int64_t cols, int64_t ld, int64_t batch,
-                      int64_t bstride, int box_rows) {
-  auto enc = tma_encoder();
-  cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows), cuuint64_t(batch)};
-  cuuint64_t strides[2] = {cuuint64_t(ld) * 8, cuuint64_t(batch > 1 ? bstride : rows * ld) * 8};
-  cuuint32_t box[3] = {16, cuuint32_t(box_rows), 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <auto KERN, int THREADS, size_t SMEM>
 inline cudaError_t launch_tma_t(const GemmTmaArgs& args, dim3 grid, cudaStream_t st) {
   static bool attr = false;
@@ -227,8 +215,8 @@ inline cudaError_t launch_dgemm_tma(const GemmProblem& pr, cudaStream_t st) {
   using LY = TmaLayout<CF>;
   GemmTmaArgs args;
   args.pr = pr;
-  if (!encode_3d(&args.mapA, pr.A, pr.N, pr.P, pr.lda, pr.batch, pr.sA, CF::BM) ||
-      !encode_3d(&args.mapB, pr.B, pr.P, pr.M, pr.ldb, pr.batch, pr.sB, 16))
+  if (!tma_encode_3d(&args.mapA, pr.A, pr.N, pr.P, pr.lda, pr.batch, pr.sA, CF::BM) ||
+      !tma_encode_3d(&args.mapB, pr.B, pr.P, pr.M, pr.ldb, pr.batch, pr.sB, 16))
     return cudaErrorInvalidValue;
   const bool cv = (reinterpret_cast<uintptr_t>(pr.C) & 15) == 0 && pr.ldc % 2 == 0 && (pr.batch == 1 || pr.sC % 2 == 0);
   const int64_t tiles = cdiv(pr.N, CF::BM) * cdiv(pr.M, CF::BN);
@@ -250,11 +238,18 @@ inline cudaError_t launch_dgemm_tma(const GemmProblem& pr, cudaStream_t st) {
 // 3 CTAs (12 warps) per SM -- 36.1 TF at 8192^3, 34.0 at 2048^3, 27.5 at 1024^3 on B200
 // (tools/tune/gemm_tune.cu, profiles/r01/gemm_tune_tma.jsonl; cuBLAS DGEMM: 35.5 at 8192^3)
 using GemmTma = GemmCfg<64, 64, 2, 2, 4, 3, 16, GEMM_TMA_GROUP_M>;
+// fewer than two waves of 64 x 64 tiles (e.g. 1024^3): 64 x 32 tiles, 2 warps of 32 x 32, 6 CTAs
+// per SM -- 28.2 vs 26.6 TF at 1024^3 (profiles/r01/gemm_tune_small.jsonl)
+using GemmTmaSmall = GemmCfg<64, 32, 2, 1, 4, 6, 16, GEMM_TMA_GROUP_M>;
 
 // K1 entry: TMA-staged kernel when the operands allow a tensor map, else the cp.async kernel
 // (same k order, bitwise the same result)
 inline cudaError_t launch_dgemm(const GemmProblem& pr, cudaStream_t st, int sms = 148) {
-  if (gemm_tma_ok(pr)) return launch_dgemm_tma<GemmTma>(pr, st);
+  if (gemm_tma_ok(pr)) {
+    const int64_t tiles = cdiv(pr.N, GemmTma::BM) * cdiv(pr.M, GemmTma::BN) * pr.batch;
+    if (tiles < 2 * 3 * int64_t(sms)) return launch_dgemm_tma<GemmTmaSmall>(pr, st);
+    return launch_dgemm_tma<GemmTma>(pr, st);
+  }
   return launch_dgemm_cpasync(pr, st, sms);
 }
 

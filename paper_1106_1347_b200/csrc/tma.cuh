@@ -11,6 +11,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace mmk {
@@ -88,21 +90,87 @@ inline bool tma_ok(const void* X, int64_t ld) {
   return (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 2 == 0 && tma_encoder() != nullptr;
 }
 
+// Encoded maps are cached (the same operands recur call after call: bench loops, Strassen levels,
+// the e2e path); a map is a pure function of (address, dims, strides, box, swizzle), so a hit
+// is valid even if the memory was freed and reallocated at the same address.
+struct TmaKey {
+  const void* p;
+  uint64_t dims[3], strides[2];
+  uint32_t box[3];
+  int rank, swizzle;
+  bool operator==(const TmaKey& o) const {
+    return p == o.p && rank == o.rank && swizzle == o.swizzle && dims[0] == o.dims[0] && dims[1] == o.dims[1] &&
+           dims[2] == o.dims[2] && strides[0] == o.strides[0] && strides[1] == o.strides[1] && box[0] == o.box[0] &&
+           box[1] == o.box[1] && box[2] == o.box[2];
+  }
+};
+
+inline bool tma_encode_key(CUtensorMap* map, const TmaKey& k) {
+  constexpr int CAP = 32;
+  static std::mutex mu;
+  static TmaKey keys[CAP];
+  static CUtensorMap maps[CAP];
+  static int used = 0, next = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (int i = 0; i < used; ++i)
+      if (keys[i] == k) {
+        *map = maps[i];
+        return true;
+      }
+  }
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {k.dims[0], k.dims[1], k.dims[2]};
+  cuuint64_t strides[2] = {k.strides[0], k.strides[1]};
+  cuuint32_t box[3] = {k.box[0], k.box[1], k.box[2]};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(k.rank), const_cast<void*>(k.p), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   k.swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  std::lock_guard<std::mutex> g(mu);
+  keys[next] = k;
+  maps[next] = *map;
+  next = (next + 1) % CAP;
+  if (used < CAP) ++used;
+  return true;
+}
+
 // 2-D map of a row-major float64 matrix: box = box_rows x box_cols doubles
 // swizzle128: box_cols must be 16 (128-byte rows); 16-byte chunk c of box row r lands at chunk c ^ (r % 8)
 inline bool tma_encode_2d(CUtensorMap* map, const double* X, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                           int box_cols, bool swizzle128) {
-  auto enc = tma_encoder();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
-  cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  TmaKey k{};
+  k.p = X;
+  k.rank = 2;
+  k.swizzle = swizzle128 ? 1 : 0;
+  k.dims[0] = uint64_t(cols);
+  k.dims[1] = uint64_t(rows);
+  k.strides[0] = uint64_t(ld) * sizeof(double);
+  k.box[0] = uint32_t(box_cols);
+  k.box[1] = uint32_t(box_rows);
+  return tma_encode_key(map, k);
+}
+
+// 3-D map {columns, rows, batch} of `batch` row-major float64 matrices bstride doubles apart;
+// box = box_rows x 16 doubles x 1, 128-byte swizzle
+inline bool tma_encode_3d(CUtensorMap* map, const double* X, int64_t rows, int64_t cols, int64_t ld, int64_t batch,
+                          int64_t bstride, int box_rows) {
+  TmaKey k{};
+  k.p = X;
+  k.rank = 3;
+  k.swizzle = 1;
+  k.dims[0] = uint64_t(cols);
+  k.dims[1] = uint64_t(rows);
+  k.dims[2] = uint64_t(batch);
+  k.strides[0] = uint64_t(ld) * 8;
+  k.strides[1] = uint64_t(batch > 1 ? bstride : rows * ld) * 8;
+  k.box[0] = 16;
+  k.box[1] = uint32_t(box_rows);
+  k.box[2] = 1;
+  return tma_encode_key(map, k);
 }
 
 }  // namespace mmk

@@ -279,7 +279,8 @@ def c4_ops():
 
 
 @pytest.mark.parametrize("method,levels", [("naive", 0), ("kahan", 0), ("winograd", 0), ("winograd_scaled", 0),
-                                           ("strassen", 2), ("strassen_winograd", 2), ("strassen_winograd", 3)])
+                                           ("strassen", 2), ("strassen_winograd", 2), ("strassen", 3),
+                                           ("strassen_winograd", 3)])
 def test_c4_sampled(method, levels, c4_ops):
     """BASELINE.json config 4 at full size, in bench.py's launch configuration: 4096 seeded
     entries + 2 full rows against the oracle's per-entry replicas (bitwise), and the inf-norm

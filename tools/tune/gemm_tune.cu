@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../paper_1106_1347_b200/csrc/gemm_tma.cuh"
@@ -58,7 +59,56 @@ void run(const char* name, const double* A, const double* B, double* C, const do
   fflush(stdout);
 }
 
+// rectangular problem N x P x M through a given path (config c3 is 4096 x 1001 x 3000)
+template <class CF, bool TMA>
+void run_rect(const char* name, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+              int reps) {
+  GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
+  auto go = [&]() { return TMA ? launch_dgemm_tma<CF>(pr, 0) : launch_dgemm_cfg<CF>(pr, 0); };
+  go();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) go();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  printf("{\"cfg\":\"%s\",\"N\":%lld,\"P\":%lld,\"M\":%lld,\"ms\":%.4f,\"tflops\":%.2f,\"err\":\"%s\"}\n", name,
+         (long long)N, (long long)P, (long long)M, ms, 2.0 * N * P * M / ms / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "c3") {
+    double *A, *B, *C;
+    cudaMalloc(&A, 4096 * 1002 * 8);
+    cudaMalloc(&B, 1002 * 3000 * 8);
+    cudaMalloc(&C, 4096 * 3000 * 8);
+    fill<<<1024, 256>>>(A, 4096 * 1002, 1);
+    fill<<<1024, 256>>>(B, 1002 * 3000, 2);
+    run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P1000", A, B, C, 4096, 1000, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_P1000", A, B, C, 4096, 1000, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_P1002", A, B, C, 4096, 1002, 3000, 20);
+    double *A2, *B2, *C2;
+    cudaMalloc(&A2, 8192ll * 8192 * 8);
+    cudaMalloc(&B2, 8192ll * 8192 * 8);
+    cudaMalloc(&C2, 8192ll * 8192 * 8);
+    fill<<<1024, 256>>>(A2, 8192ll * 8192, 1);
+    fill<<<1024, 256>>>(B2, 8192ll * 8192, 2);
+    run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 4>, false>("cpasync_64x64_s3_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
+    return 0;
+  }
   int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
   int reps = argc > 2 ? atoi(argv[2]) : 3;
   double *A, *B, *C, *R;
@@ -70,11 +120,11 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 8>, true>("tma_64x64_s4_3cta_g8", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 4>, true>("tma_64x64_s4_3cta_g4", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 16>, true>("tma_64x64_s4_3cta_g16", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 21>, true>("tma_64x64_s4_3cta_g21", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 32>, true>("tma_64x64_s4_3cta_g32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3, 16, 8>, true>("tma_64x64_s4_3cta_g8_again", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<64, 32, 2, 1, 4, 6>, true>("tma_64x32_w2x1_s4_6cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<32, 64, 1, 2, 4, 6>, true>("tma_32x64_w1x2_s4_6cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<32, 32, 1, 1, 4, 10>, true>("tma_32x32_w1x1_s4_10cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 32, 2, 1, 6, 4>, true>("tma_64x32_w2x1_s6_4cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<32, 64, 2, 2, 4, 6>, true>("tma_32x64_w2x2_s4_6cta", A, B, C, R, n, reps, bad);
   return 0;
 }

@@ -89,7 +89,48 @@ void wino_tma(const char* name, Ctx& c) {
     launch_winograd_pairs_tma<CF, false>(c.A, c.B, c.C, c.y, c.z, c.n, c.n, c.n, 0);
   }, 2.0);
 }
+// c3-shaped rectangular runs (odd P = 1001: cp.async paths)
+template <class CF>
+void rect(const char* kind, const char* name, const double* A, const double* B, double* C, double* y, double* z,
+          int64_t N, int64_t P, int64_t M) {
+  auto go = [&]() {
+    if (kind[0] == 'k') launch_kahan<CF>(A, B, C, N, P, M, 0);
+    else launch_winograd<CF>(A, B, C, y, z, N, P, M, 0);
+  };
+  go();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 10; ++r) go();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("{\"kernel\":\"%s\",\"cfg\":\"%s\",\"N\":%lld,\"P\":%lld,\"M\":%lld,\"ms\":%.4f,\"err\":\"%s\"}\n", kind,
+         name, (long long)N, (long long)P, (long long)M, ms / 10, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'c') {
+    double *A, *B, *C, *y, *z;
+    cudaMalloc(&A, 4096 * 1002 * 8);
+    cudaMalloc(&B, 1002 * 3000 * 8);
+    cudaMalloc(&C, 4096 * 3000 * 8);
+    cudaMalloc(&y, 4096 * 8);
+    cudaMalloc(&z, 3000 * 8);
+    fill<<<1024, 256>>>(A, 4096 * 1002, 1);
+    fill<<<1024, 256>>>(B, 1002 * 3000, 2);
+    rect<SimtCfg<128, 64, 8, 8, 3, 2>>("winograd", "128x64_t8x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<64, 64, 4, 8, 3, 2>>("winograd", "64x64_t4x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<64, 64, 8, 8, 3, 4>>("winograd", "64x64_t8x8_s3_4cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<64, 64, 4, 8, 3, 2>>("kahan", "64x64_t4x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<64, 64, 8, 4, 3, 2>>("kahan", "64x64_t8x4_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<32, 64, 4, 8, 3, 3>>("kahan", "32x64_t4x8_s3_3cta", A, B, C, y, z, 4096, 1001, 3000);
+    return 0;
+  }
   Ctx c;
   c.n = argc > 1 ? atoll(argv[1]) : 8192;
   c.reps = argc > 2 ? atoi(argv[2]) : 2;
