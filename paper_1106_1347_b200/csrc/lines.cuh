@@ -124,7 +124,9 @@ __device__ __forceinline__ void ln_issue(const LineLaunch& L, int ji, double* t,
   }
 }
 
-template <int OP>
+// SCALED: the jobs carry scale_sel >= 0 (WinogradScaled's copies); a compile-time flag so the
+// unscaled y/z pass executes exactly the method's DMUL/DADD (SASS fingerprint, tools/fingerprint.py)
+template <int OP, bool SCALED>
 __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ LineLaunch L) {
   extern __shared__ __align__(1024) unsigned char ln_raw[];
   // 1024-byte aligned stage buffers (the 128-byte swizzle pattern repeats every 1024 bytes)
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   const int64_t KT = cdiv(jb.len, LN_TK);
 
   double s = 1.0;
-  if (jb.scale_sel >= 0) {
+  if (SCALED && jb.scale_sel >= 0) {
     const double nA = __longlong_as_double(static_cast<long long>(L.norms[0]));
     const double nB = __longlong_as_double(static_cast<long long>(L.norms[1]));
     const int lam = lambda_rule(nA, nB);
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   for (int st = 0; st < LN_STAGES; ++st)
     if (st < KT) ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, st, lane);
 
-  const bool scaled = jb.scale_sel >= 0;
+  const bool scaled = SCALED && jb.scale_sel >= 0;
   double acc = 0.0;
 #pragma unroll 1
   for (int64_t kt = 0; kt < KT; ++kt) {
@@ -288,11 +290,12 @@ inline void ln_finish_job(LineJob& j, CUtensorMap* map) {
   }
 }
 
-template <int OP>
+template <int OP, bool SCALED = false>
 inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(line_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LN_SMEM));
+    cudaError_t e =
+        cudaFuncSetAttribute(line_kernel<OP, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LN_SMEM));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -301,7 +304,7 @@ inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
     ln_finish_job(L.job[i], &L.map[i]);
     blocks += L.job[i].blocks;
   }
-  line_kernel<OP><<<unsigned(blocks), LN_LINES, LN_SMEM, st>>>(L);
+  line_kernel<OP, SCALED><<<unsigned(blocks), LN_LINES, LN_SMEM, st>>>(L);
   note_launch();
   return cudaGetLastError();
 }
@@ -361,7 +364,8 @@ inline cudaError_t launch_yz(const double* A, const double* B, double* y, double
     L.job[1].copy = Bs;
     L.job[1].scale_sel = 1;
   }
-  return fused ? launch_lines<LN_PAIRS_FMA>(L, st) : launch_lines<LN_PAIRS>(L, st);
+  if (scaled) return fused ? launch_lines<LN_PAIRS_FMA, true>(L, st) : launch_lines<LN_PAIRS, true>(L, st);
+  return fused ? launch_lines<LN_PAIRS_FMA, false>(L, st) : launch_lines<LN_PAIRS, false>(L, st);
 }
 
 }  // namespace mmk

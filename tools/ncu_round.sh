@@ -22,3 +22,8 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
     --clock-control none -k regex:"strassen_form|strassen_combine|line_kernel" --csv \
     --log-file $OUT/hbm_kernels.csv $QB > $OUT/ncu_hbm.log 2>&1
 echo "hbm rc=$?"
+# SASS instruction fingerprints of every method (DADD / DMUL / DFMA / DMMA counts)
+python tools/fingerprint.py run > $OUT/plain_fp.log 2>&1 && \
+ncu --metrics $(python tools/fingerprint.py metrics) --csv --log-file $OUT/fingerprint.csv \
+    python tools/fingerprint.py run > $OUT/ncu_fp.log 2>&1
+echo "fingerprint rc=$?"

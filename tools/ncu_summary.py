@@ -18,9 +18,9 @@ def short(name: str) -> str:
 
 
 def family(name: str) -> str:
-    if "line_kernel<0>" in name:
+    if "line_kernel<0" in name:
         return "line_kernel<0> (norm_inf)"
-    if "line_kernel<1>" in name:
+    if "line_kernel<1" in name or "line_kernel<2" in name:
         return "line_kernel<1> (winograd y/z)"
     for k in ("dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
               "winograd_kernel",
