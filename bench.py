@@ -59,6 +59,8 @@ def parse_args():
     ap.add_argument("--methods", default=",".join(METHODS))
     ap.add_argument("--panels", type=int, default=8,
                     help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="N > 1 collectives (gloo only to exercise the multi-rank path on fewer GPUs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -208,7 +210,7 @@ def config_dict(args, cfg, world):
         "workload": f"{cfg.key}: A {cfg.N}x{cfg.P}, B {cfg.P}x{cfg.M} float64 ({cfg.dist}), one call of each of "
                     f"{args.methods.replace(',', ', ')} per step",
         "N": cfg.N, "P": cfg.P, "M": cfg.M, "strassen_levels": args.levels,
-        "parallelism": (f"row-block dp{world} (B broadcast via NCCL; naive: {args.panels} k-panels overlapped)"
+        "parallelism": (f"row-block dp{world} (B broadcast via {args.dist_backend}; naive: {args.panels} k-panels overlapped)"
                         if world > 1 else "1 GPU"),
         "l2": "inputs larger than L2 (A, B, C = 537 MB each vs 126 MB L2)" if cfg.N >= 4096
         else "inputs smaller than L2 (not flushed)",
@@ -226,10 +228,13 @@ def run_mine(args):
     from paper_1106_1347_b200 import dist as mmdist
 
     rank, world, local = env_rank()
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # host-staged collectives: lets the N > 1 code path run with several ranks on one GPU (tests)
+            dist.init_process_group(args.dist_backend)
     cfg = workload.CONFIGS[args.config]
     methods = tuple(args.methods.split(","))
     N, P, M = cfg.N, cfg.P, cfg.M
