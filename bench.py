@@ -396,13 +396,15 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M):
         if world == 1:
             mm.matmul_methods(hA, hB, order, levels=args.levels, outs=houts)
             return
+        # N > 1: each rank's rows of A (and B on the root) copied once per step; every product
+        # broadcasts B inside dist_gemm and its C rows come back to the host
+        dA = hA.to(dev, non_blocking=True)
+        if rank == 0:
+            dB.copy_(hB, non_blocking=True)
         for m in methods:
-            dA = hA.to(dev, non_blocking=True)
-            if rank == 0:
-                dB.copy_(hB, non_blocking=True)
             C = mmdist.dist_gemm(m, dA, dB, levels=args.levels, panels=args.panels)
             hC.copy_(C, non_blocking=True)
-            stream.synchronize()
+        stream.synchronize()
 
     step()
     torch.cuda.synchronize()
@@ -424,16 +426,14 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M):
 
     cfgN = CONFIGS[args.config].N
     flop = 2.0 * cfgN * P * M * len(methods)
-    if world == 1:
-        h2d = 8 * (n_loc * P + P * M)  # A and B once per step
-    else:
-        h2d = len(methods) * 8 * (n_loc * P + (P * M if rank == 0 else 0))
+    h2d = 8 * (n_loc * P + (P * M if rank == 0 else 0))  # A (this rank's rows) and B (root) once per step
     d2h = len(methods) * 8 * n_loc * M
     return {"value": round(flop / (ms / 1e3) / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": steps,
             "path": "paper_1106_1347_b200.matmul_methods on pinned host tensors (per step: H2D A, B once; every "
                     "method's C D2H, overlapped with the next method)"
-            if world == 1 else "dist_gemm with per-rank H2D of its A rows (+B on root) and D2H of its C rows"}
+            if world == 1 else "dist_gemm: per step H2D of each rank's A rows (+ B on the root) once, every method's "
+                               "C rows D2H"}
 
 
 def main():
