@@ -18,6 +18,24 @@ inline std::atomic<uint64_t>& launch_counter() {
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
+// Opt kernel KERN into `bytes` of dynamic shared memory on the CURRENT device, once per
+// (kernel, device): the attribute is per device, so a process driving several GPUs needs it on each.
+template <auto KERN>
+inline cudaError_t smem_attr_once(size_t bytes) {
+  constexpr int kMaxDev = 64;
+  static std::atomic<bool> done[kMaxDev];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!done[dev].load(std::memory_order_acquire)) {
+    e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+    done[dev].store(true, std::memory_order_release);
+  }
+  return cudaSuccess;
+}
+
 // ---- asynchronous global -> shared copies (LDGSTS).  src_size = 0 zero-fills the
 // destination without reading global memory (used for out-of-range tile elements).
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {

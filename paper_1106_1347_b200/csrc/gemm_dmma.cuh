@@ -210,13 +210,9 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_dmma_kernel
 // ---- host-side launcher ------------------------------------------------------
 template <class CF, int AV, int BV, int CV>
 cudaError_t launch_dgemm_t(const GemmProblem& pr, cudaStream_t st) {
-  auto kern = dgemm_dmma_kernel<CF, AV, BV, CV>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  constexpr auto kern = dgemm_dmma_kernel<CF, AV, BV, CV>;
+  cudaError_t e = smem_attr_once<kern>(CF::SMEM);
+  if (e != cudaSuccess) return e;
   const int64_t tiles = cdiv(pr.N, CF::BM) * cdiv(pr.M, CF::BN);
   dim3 grid(unsigned(tiles), 1, 1);
   if (pr.batch <= 65535) {

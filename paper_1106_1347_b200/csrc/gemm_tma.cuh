@@ -199,12 +199,8 @@ inline bool gemm_tma_ok(const GemmProblem& pr) {
 
 template <auto KERN, int THREADS, size_t SMEM>
 inline cudaError_t launch_tma_t(const GemmTmaArgs& args, dim3 grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr_once<KERN>(SMEM);
+  if (e != cudaSuccess) return e;
   KERN<<<grid, THREADS, SMEM, st>>>(args);
   note_launch();
   return cudaGetLastError();

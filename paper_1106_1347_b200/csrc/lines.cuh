@@ -292,13 +292,8 @@ inline void ln_finish_job(LineJob& j, CUtensorMap* map) {
 
 template <int OP, bool SCALED = false>
 inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(line_kernel<OP, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LN_SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr_once<line_kernel<OP, SCALED>>(LN_SMEM);
+  if (e != cudaSuccess) return e;
   int blocks = 0;
   for (int i = 0; i < L.njobs; ++i) {
     ln_finish_job(L.job[i], &L.map[i]);

@@ -264,12 +264,8 @@ inline bool simt_tma_ok(const double* A, const double* B, int64_t N, int64_t P, 
 
 template <auto KERN, int THREADS, size_t SMEM>
 inline cudaError_t launch_simt_tma_t_(const SimtTmaArgs& args, unsigned grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr_once<KERN>(SMEM);
+  if (e != cudaSuccess) return e;
   KERN<<<grid, THREADS, SMEM, st>>>(args);
   note_launch();
   return cudaGetLastError();

@@ -138,13 +138,9 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 template <class CF, int AV, int BV, int CV, bool FUSED>
 cudaError_t launch_winograd_t(const double* A, const double* B, double* C, const double* y, const double* z,
                               int64_t N, int64_t P, int64_t M, cudaStream_t st) {
-  auto kern = winograd_kernel<CF, AV, BV, CV, FUSED>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  constexpr auto kern = winograd_kernel<CF, AV, BV, CV, FUSED>;
+  cudaError_t e = smem_attr_once<kern>(CF::SMEM);
+  if (e != cudaSuccess) return e;
   dim3 grid(unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM)));
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(A, B, C, y, z, N, P, M);
   note_launch();
