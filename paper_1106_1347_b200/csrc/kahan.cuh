@@ -16,8 +16,9 @@
 
 namespace mmk {
 
-// 64 x 64 tiles, 128 threads of 4 x 8 outputs, 2 CTAs per SM (tools/tune/simt_tune.cu)
-using KahanDefault = SimtCfg<64, 64, 4, 8, 3, 2>;
+// 64 x 64 x 32 tiles, 128 threads of 4 x 8 outputs, double-buffered, 2 CTAs per SM
+// (tools/tune/simt_tune.cu; 157.5 vs 158.0 ms for 16-deep k tiles, profiles/r01/simt_tune_bk32.jsonl)
+using KahanDefault = SimtCfg<64, 64, 4, 8, 2, 2, 32>;
 
 // FUSED (NEXT-3, reading R22): err = fma(a, b, err) replaces x = a*b; err = err + x
 template <class CF, bool FUSED>

@@ -5,11 +5,13 @@
 
 namespace mmk {
 
-// CTA tile BM x BN x 16, thread tile TM x TN, STAGES-deep cp.async ring, MINB CTAs per SM.
-template <int BM_, int BN_, int TM_, int TN_, int STAGES_, int MINB_>
+// CTA tile BM x BN x BK, thread tile TM x TN, STAGES-deep cp.async ring, MINB CTAs per SM.
+// A rows are padded to BK + 2 doubles: (BK + 2) / 2 16-byte units is odd for BK = 16, 32, so the
+// row reads of the 4 thread rows of a warp fall in distinct banks.
+template <int BM_, int BN_, int TM_, int TN_, int STAGES_, int MINB_, int BK_ = 16>
 struct SimtCfg {
   static constexpr int BM = BM_, BN = BN_, TM = TM_, TN = TN_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr int BK = 16, APITCH = BK + 2;
+  static constexpr int BK = BK_, APITCH = BK + 2;
   static constexpr int TXN = BN / TN, TYM = BM / TM, THREADS = TXN * TYM;
   static constexpr int A_ELEMS = BM * APITCH, B_ELEMS = BK * BN;
   static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
@@ -27,7 +29,7 @@ __device__ __forceinline__ void simt_load_tile(double* As, double* Bs, const dou
 #pragma unroll
     for (int i = 0; i < (CF::BM * BK / 2) / T; ++i) {
       int c = tid + i * T;
-      int r = c >> 3, kp = (c & 7) * 2;
+      int r = c / (BK / 2), kp = (c % (BK / 2)) * 2;
       int64_t gm = m0 + r, gk = k0 + kp;
       bool v = gm < N && gk < kend;
       cp_async16(As + r * AP + kp, v ? A + gm * P + gk : A, v);
@@ -36,7 +38,7 @@ __device__ __forceinline__ void simt_load_tile(double* As, double* Bs, const dou
 #pragma unroll
     for (int i = 0; i < (CF::BM * BK) / T; ++i) {
       int e = tid + i * T;
-      int r = e >> 4, kk = e & 15;
+      int r = e / BK, kk = e % BK;
       int64_t gm = m0 + r, gk = k0 + kk;
       bool v = gm < N && gk < kend;
       cp_async8(As + r * AP + kk, v ? A + gm * P + gk : A, v);

@@ -143,18 +143,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&c.bad, 8);
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
-  // SimtCfg<BM, BN, TM, TN, STAGES, MINB>
-  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_t8x8_s3_2cta", c, true);
-  wino_tma<SimtCfg<128, 64, 8, 8, 3, 2>>("tma_128x64_t8x8_s3_2cta", c);
+  // SimtCfg<BM, BN, TM, TN, STAGES, MINB, BK>
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("cpasync_64x64_t4x8_s3_2cta_bk16", c, true);
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("cpasync_64x64_t4x8_s3_2cta_bk32", c, false);
+  kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_t4x8_s2_2cta_bk32", c, false);
+  kahan<SimtCfg<64, 64, 8, 4, 3, 2, 32>>("cpasync_64x64_t8x4_s3_2cta_bk32", c, false);
+  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("cpasync_64x64_t4x8_s3_2cta_bk16_again", c, false);
+  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_t8x8_s3_2cta_bk16", c, true);
+  wino<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("cpasync_128x64_t8x8_s2_2cta_bk32", c, false);
   wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_t8x8_s4_2cta", c);
-  wino_tma<SimtCfg<64, 64, 8, 8, 4, 4>>("tma_64x64_t8x8_s4_4cta", c);
-  wino_tma<SimtCfg<64, 64, 4, 8, 4, 2>>("tma_64x64_t4x8_s4_2cta", c);
-  wino_tma<SimtCfg<64, 64, 4, 8, 4, 3>>("tma_64x64_t4x8_s4_3cta", c);
-  kahan<SimtCfg<64, 64, 4, 8, 3, 2>>("cpasync_64x64_t4x8_s3_2cta", c, true);
-  kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2>>("tma_64x64_t4x8_s3_2cta", c);
-  kahan_tma<SimtCfg<64, 64, 4, 8, 4, 2>>("tma_64x64_t4x8_s4_2cta", c);
-  kahan_tma<SimtCfg<64, 64, 4, 8, 6, 2>>("tma_64x64_t4x8_s6_2cta", c);
-  kahan_tma<SimtCfg<64, 64, 4, 8, 4, 3>>("tma_64x64_t4x8_s4_3cta", c);
-  kahan_tma<SimtCfg<128, 64, 4, 8, 4, 1>>("tma_128x64_t4x8_s4_1cta", c);
   return 0;
 }
