@@ -14,6 +14,8 @@
 #pragma once
 #include "simt_tile.cuh"
 
+#include <type_traits>
+
 namespace mmk {
 
 // 64 x 64 x 32 tiles, 128 threads of 4 x 8 outputs, double-buffered, 2 CTAs per SM
@@ -123,15 +125,30 @@ cudaError_t launch_kahan_t(const double* A, const double* B, double* C, int64_t 
   return cudaGetLastError();
 }
 
-template <class CF = KahanDefault, bool FUSED = false>
-inline cudaError_t launch_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
-                                cudaStream_t st) {
+template <class CF, bool FUSED>
+inline cudaError_t launch_kahan_cfg(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                                    cudaStream_t st) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool av = al(A) && P % 2 == 0, bv = al(B) && M % 2 == 0, cv = al(C) && M % 2 == 0;
   if (av && bv && cv) return launch_kahan_t<CF, 2, 2, 2, FUSED>(A, B, C, N, P, M, st);
   if (bv && cv) return launch_kahan_t<CF, 1, 2, 2, FUSED>(A, B, C, N, P, M, st);
   if (av) return launch_kahan_t<CF, 2, 1, 1, FUSED>(A, B, C, N, P, M, st);
   return launch_kahan_t<CF, 1, 1, 1, FUSED>(A, B, C, N, P, M, st);
+}
+
+// fewer 64 x 64 tiles than the two CTA slots per SM (e.g. 1024^3): 32 x 32 tiles, 64 threads of
+// 2 x 4 outputs, 4 CTAs per SM -- 0.351 vs 0.373 ms at 1024^3 (profiles/r01/simt_tune_small.jsonl)
+using KahanSmall = SimtCfg<32, 32, 2, 4, 3, 4>;
+
+template <class CF = void, bool FUSED = false>
+inline cudaError_t launch_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                                cudaStream_t st, int sms = 148) {
+  if (!std::is_void<CF>::value)
+    return launch_kahan_cfg<typename std::conditional<std::is_void<CF>::value, KahanDefault, CF>::type, FUSED>(
+        A, B, C, N, P, M, st);
+  if (cdiv(N, KahanDefault::BM) * cdiv(M, KahanDefault::BN) < 2 * int64_t(sms))
+    return launch_kahan_cfg<KahanSmall, FUSED>(A, B, C, N, P, M, st);
+  return launch_kahan_cfg<KahanDefault, FUSED>(A, B, C, N, P, M, st);
 }
 
 }  // namespace mmk

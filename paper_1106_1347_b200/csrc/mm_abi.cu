@@ -123,15 +123,17 @@ int mm_naive_ex(const double* A, int64_t lda, const double* B, int64_t ldb, doub
 int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
-  if ((rc = check_device(nullptr))) return rc;
-  return cuda_status(mmk::launch_kahan(A, B, C, N, P, M, S(stream)));
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
+  return cuda_status(mmk::launch_kahan(A, B, C, N, P, M, S(stream), sms));
 }
 
 int mm_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
-  if ((rc = check_device(nullptr))) return rc;
-  return cuda_status(mmk::launch_kahan<mmk::KahanDefault, true>(A, B, C, N, P, M, S(stream)));
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
+  return cuda_status(mmk::launch_kahan<void, true>(A, B, C, N, P, M, S(stream), sms));
 }
 
 size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels) {
