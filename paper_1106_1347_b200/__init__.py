@@ -354,14 +354,31 @@ def matmul(A: torch.Tensor, B: torch.Tensor, method: str = "naive", *, levels: i
     return out
 
 
+def _h2d_2d(dA: torch.Tensor, hA: torch.Tensor, k0: int, k1: int, stream) -> None:
+    """dA[:, k0:k1] <- hA[:, k0:k1] (pinned host, row-major) as ONE strided 2-D copy on `stream`
+    (cudaMemcpy2DAsync through the CUDA runtime bindings; torch would gather a strided pinned
+    source through a pageable temporary, which is synchronous)."""
+    from cuda.bindings import runtime as rt
+
+    pitch = hA.stride(0) * 8
+    err, = rt.cudaMemcpy2DAsync(dA.data_ptr() + k0 * 8, dA.stride(0) * 8, hA.data_ptr() + k0 * 8, pitch,
+                                (k1 - k0) * 8, hA.shape[0], rt.cudaMemcpyKind.cudaMemcpyHostToDevice,
+                                stream.cuda_stream)
+    if err != rt.cudaError_t.cudaSuccess:
+        raise MMError(f"cudaMemcpy2DAsync failed: {err}")
+
+
 def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2, device=None,
                    outs: Optional[dict] = None, row_blocks: int = 4) -> dict:
     """The shape of the paper's test program: several methods applied to the
     SAME host operands.  A and B (pinned host float64) are copied to the device once; every
     method's product is copied back into outs[method] (pinned host, allocated if missing) on a
-    copy stream while the next method computes.  When the first method is row-local its row
-    blocks start as soon as their rows of A have landed; when the last one is, its result
-    streams back by row blocks.  Each product is bitwise the one-shot device call's."""
+    copy stream while the next method computes.  When the first method is NaivStandard, A and B
+    travel in k-panels (A's column panels as 2-D copies) and the product accumulates panel by
+    panel as they land (mm_naive_ex, reading R23: bitwise the one-shot chain); when it is another
+    row-local method its row blocks start as soon as their rows of A have landed.  When the last
+    method is row-local its result streams back by row blocks.  Each product is bitwise the
+    one-shot device call's."""
     methods = list(methods)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     s = torch.cuda.current_stream(dev)
@@ -374,17 +391,31 @@ def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2
             outs[m] = torch.empty((N, M), dtype=torch.float64, pin_memory=True)
     rb = max(1, min(row_blocks, N // 2)) if N >= 2 else 1
     bounds = [(N * b) // rb for b in range(rb + 1)]
+    k_panels = None
+    if methods and methods[0] == "naive" and A.is_pinned() and B.is_pinned() and A.is_contiguous() and P >= 4:
+        from .dist import panel_bounds
+
+        k_panels = panel_bounds(P, row_blocks)
     s_in.wait_stream(s)
     with torch.cuda.stream(s_in):
-        dB = B.to(dev, non_blocking=True)
         dA = torch.empty((N, P), dtype=torch.float64, device=dev)
+        dB = torch.empty((P, M), dtype=torch.float64, device=dev)
         a_ready = []
-        for b in range(rb):
-            lo, hi = bounds[b], bounds[b + 1]
-            dA[lo:hi].copy_(A[lo:hi], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(s_in)
-            a_ready.append(ev)
+        if k_panels is not None:
+            for k0, k1 in k_panels:  # A[:, k0:k1] (strided) and B[k0:k1] (contiguous)
+                _h2d_2d(dA, A, k0, k1, s_in)
+                dB[k0:k1].copy_(B[k0:k1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_in)
+                a_ready.append(ev)
+        else:
+            dB.copy_(B, non_blocking=True)
+            for b in range(rb):
+                lo, hi = bounds[b], bounds[b + 1]
+                dA[lo:hi].copy_(A[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_in)
+                a_ready.append(ev)
     bufs = [torch.empty((N, M), dtype=torch.float64, device=dev) for _ in range(min(2, len(methods)))]
     buf_free = [None] * len(bufs)
     for i, m in enumerate(methods):
@@ -396,10 +427,17 @@ def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2
         buf = bufs[k]
         row_local = m in _ROW_LOCAL and rb > 1
         first, last = i == 0, i == len(methods) - 1
-        if row_local and (first or last):
+        if first and k_panels is not None:  # NaivStandard accumulating k-panels as they land
+            for j, (k0, k1) in enumerate(k_panels):
+                s.wait_event(a_ready[j])
+                naive_panel(dA[:, k0:k1], dB[k0:k1], buf, accumulate=j > 0, stream=s)
+            s_out.wait_stream(s)
+            with torch.cuda.stream(s_out):
+                outs[m].copy_(buf, non_blocking=True)
+        elif row_local and (first or last):
             for b in range(rb):
                 lo, hi = bounds[b], bounds[b + 1]
-                s.wait_event(a_ready[b])
+                s.wait_event(a_ready[b] if k_panels is None else a_ready[-1])
                 f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
                 s_out.wait_stream(s)
                 with torch.cuda.stream(s_out):

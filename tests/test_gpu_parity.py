@@ -387,9 +387,12 @@ def test_matmul_methods_bitwise():
     A, B = workload.custom(517, 130, 258, seed=12)
     hA = torch.from_numpy(A).pin_memory()
     hB = torch.from_numpy(B).pin_memory()
-    order = ["naive", "strassen", "winograd_scaled", "winograd", "kahan"]
-    outs = mm.matmul_methods(hA, hB, order, levels=1)
     dA, dB = dev(A), dev(B)
-    for m in order:
-        ref = host(run(m, dA, dB, 1))
-        assert np.array_equal(outs[m].numpy(), ref), m
+    # naive first: k-panel pipeline (2-D copies of A's column panels + accumulate-mode GEMM);
+    # kahan first: row-block pipeline; a row-local method last: row-block D2H
+    for order in (["naive", "strassen", "winograd_scaled", "winograd", "kahan"],
+                  ["kahan", "strassen_winograd", "naive"]):
+        outs = mm.matmul_methods(hA, hB, order, levels=1)
+        for m in order:
+            ref = host(run(m, dA, dB, 1))
+            assert np.array_equal(outs[m].numpy(), ref), (order, m)
