@@ -330,7 +330,8 @@ def run_mine(args):
     n_eff = n_loc
     kernels = {
         "naive": ("tensor", 2.0 * n_eff * P * M, peaks["dmma_tflops"], "dgemm_tma_kernel"),
-        "kahan": ("alu", 5.0 * n_eff * P * M, peaks["simt_op_tflops"], "kahan_gemm_kernel"),
+        "kahan": ("alu", 5.0 * n_eff * P * M, peaks["simt_op_tflops"],
+                  "kahan_tma_kernel" if P % 2 == 0 and M % 2 == 0 else "kahan_gemm_kernel"),
         "winograd": ("alu", 4.0 * n_eff * M * (P // 2), peaks["simt_op_tflops"],
                      "winograd_tma_kernel" if P % 2 == 0 and M % 2 == 0 else "winograd_kernel"),
     }

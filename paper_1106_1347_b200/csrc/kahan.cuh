@@ -13,6 +13,7 @@
 // stops exactly at P (padded terms are NOT no-ops for the compensated update).
 #pragma once
 #include "simt_tile.cuh"
+#include "simt_tma.cuh"
 
 #include <type_traits>
 
@@ -139,6 +140,9 @@ inline cudaError_t launch_kahan_cfg(const double* A, const double* B, double* C,
 // fewer 64 x 64 tiles than the two CTA slots per SM (e.g. 1024^3): 32 x 32 tiles, 64 threads of
 // 2 x 4 outputs, 4 CTAs per SM -- 0.351 vs 0.373 ms at 1024^3 (profiles/r01/simt_tune_small.jsonl)
 using KahanSmall = SimtCfg<32, 32, 2, 4, 3, 4>;
+// TMA-fed main loop (simt_tma.cuh) for 16-byte aligned operands with P, M even: 64 x 64 x 32
+// tiles, 3 stages -- 157.0 vs 157.5 ms at 8192^3 (profiles/r01/simt_tune_tma_bk32.jsonl)
+using KahanTma = SimtCfg<64, 64, 4, 8, 3, 2, 32>;
 
 template <class CF = void, bool FUSED = false>
 inline cudaError_t launch_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
@@ -148,6 +152,7 @@ inline cudaError_t launch_kahan(const double* A, const double* B, double* C, int
         A, B, C, N, P, M, st);
   if (cdiv(N, KahanDefault::BM) * cdiv(M, KahanDefault::BN) < 2 * int64_t(sms))
     return launch_kahan_cfg<KahanSmall, FUSED>(A, B, C, N, P, M, st);
+  if (simt_tma_ok(A, B, N, P, M)) return launch_kahan_tma<KahanTma, FUSED>(A, B, C, N, P, M, st);
   return launch_kahan_cfg<KahanDefault, FUSED>(A, B, C, N, P, M, st);
 }
 

@@ -1,13 +1,14 @@
 // simt_tma.cuh -- TMA-fed main loops of the FP64 SIMT kernels: K2 Kahan and
 // K3 Winograd pair sums, for operands a tensor map can describe (16-byte aligned,
 // even pitches: P and M even).  Other operands use the cp.async kernels of kahan.cuh /
-// winograd.cuh.  Measured at 8192^3 (profiles/r01/simt_tune_tma.jsonl): Winograd 65.6 ms vs
-// 67.4 ms with cp.async -> the product path; Kahan 161.7 ms vs 157.8 ms -> kept for the tuning
-// harness only (the swizzled address arithmetic costs more than the barriers it removes).
+// winograd.cuh.  Measured at 8192^3 with 32-deep k tiles (profiles/r01/simt_tune_tma_bk32.jsonl):
+// Winograd 65.1 ms vs 67.4 ms with cp.async, Kahan 157.0 ms vs 157.5 ms.  (With 16-deep tiles
+// the TMA Kahan lost, 161.7 vs 157.8 ms: the swizzled addressing cost more than the barriers it
+// removed; profiles/r01/simt_tune_tma.jsonl.)
 // Per output entry the arithmetic and its order are exactly those kernels' (and the
 // oracle's): only the operand staging differs, so results are bitwise identical.
 //
-//  * A tile = one TMA box [BM rows][16 k], B tile = BN/16 boxes [16 k][16 columns], 128-byte
+//  * A tile = BK/16 TMA boxes [BM rows][16 k], B tile = BN/16 boxes [BK k][16 columns], 128-byte
 //    swizzle (16-byte chunk q of box row r at chunk q ^ (r % 8)).  Thread (ty, tx) reads rows
 //    ty + TYM i of A (4 consecutive rows per warp -> 4 distinct chunks, broadcast over tx) and
 //    the column pairs 2 tx + 16 c of B (box c, chunk tx -> 8 distinct chunks): conflict free.
@@ -35,17 +36,23 @@ struct SimtTmaArgs {
 
 template <class CF>
 struct SimtTmaLayout {
-  static constexpr int A_TILE = CF::BM * 16, B_TILE = 16 * CF::BN;
+  static constexpr int A_TILE = CF::BM * CF::BK, B_TILE = CF::BK * CF::BN;
   static constexpr unsigned STAGE_BYTES = unsigned(A_TILE + B_TILE) * 8u;
   static constexpr size_t SMEM = 1024 + size_t(CF::STAGES) * STAGE_BYTES + 2 * CF::STAGES * 8;
   static_assert(CF::TXN == 8, "a warp's 8 column pairs must fill one 16-column TMA box row");
-  static_assert(CF::BK == 16, "tiles of 16 k");
+  static_assert(CF::BK == 16 || CF::BK == 32, "tiles of 16 or 32 k (one or two 128-byte swizzle rows)");
 };
 
-// A[row][k] in the swizzled [BM][16] box
-__device__ __forceinline__ int sw_a(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7))) << 1) + (k & 1); }
-// B[k][2 tx + 16 c .. +1] (a 16-byte pair) in box c of [16][16]
-__device__ __forceinline__ int sw_b(int k, int tx, int c) { return c * 256 + k * 16 + ((tx ^ (k & 7)) << 1); }
+// A[row][k] in the swizzled boxes [k/16][BM][16]
+template <class CF>
+__device__ __forceinline__ int sw_a(int row, int k) {
+  return (k >> 4) * (CF::BM * 16) + row * 16 + (((((k & 15) >> 1) ^ (row & 7))) << 1) + (k & 1);
+}
+// B[k][2 tx + 16 c .. +1] (a 16-byte pair) in box c of [BK][16]
+template <class CF>
+__device__ __forceinline__ int sw_b(int k, int tx, int c) {
+  return c * (CF::BK * 16) + k * 16 + ((tx ^ (k & 7)) << 1);
+}
 
 template <class CF>
 struct SimtPipe {
@@ -68,10 +75,12 @@ struct SimtPipe {
   }
   __device__ __forceinline__ void issue(const SimtTmaArgs& a, int kt, int s) {
     mbar_arrive_expect_tx(full + s, LY::STAGE_BYTES);
-    tma_load_2d(As_base + s * LY::A_TILE, &a.mapA, kt * 16, m0, full + s);
+#pragma unroll
+    for (int h = 0; h < CF::BK / 16; ++h)
+      tma_load_2d(As_base + s * LY::A_TILE + h * (CF::BM * 16), &a.mapA, kt * CF::BK + 16 * h, m0, full + s);
 #pragma unroll
     for (int c = 0; c < CF::BN / 16; ++c)
-      tma_load_2d(Bs_base + s * LY::B_TILE + c * 256, &a.mapB, n0 + 16 * c, kt * 16, full + s);
+      tma_load_2d(Bs_base + s * LY::B_TILE + c * (CF::BK * 16), &a.mapB, n0 + 16 * c, kt * CF::BK, full + s);
   }
   // barriers + prologue; every thread calls it
   __device__ __forceinline__ void start(const SimtTmaArgs& a) {
@@ -109,8 +118,8 @@ struct SimtPipe {
   }
 };
 
-// ---------------------------------------------------------------- K2 Kahan, TMA-fed (tuning harness)
-template <class CF, int CV>
+// ---------------------------------------------------------------- K2 Kahan, TMA-fed
+template <class CF, int CV, bool FUSED>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const __grid_constant__ SimtTmaArgs a) {
   using LY = SimtTmaLayout<CF>;
   extern __shared__ __align__(1024) unsigned char k_raw[];
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
   int64_t m0, n0;
   simt_tile_coords(a.N, a.M, CF::BM, CF::BN, m0, n0);
   SimtPipe<CF> pp;
-  pp.init(k_raw, int(m0), int(n0), int(cdiv(a.P, 16)));
+  pp.init(k_raw, int(m0), int(n0), int(cdiv(a.P, CF::BK)));
   pp.start(a);
 
   double sum[CF::TM][CF::TN], err[CF::TM][CF::TN];
@@ -130,10 +139,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
   auto step = [&](const double* As, const double* Bs, int kk) {
     double av[CF::TM], bv[CF::TN];
 #pragma unroll
-    for (int i = 0; i < CF::TM; ++i) av[i] = As[sw_a(simt_row<CF>(ty, i), kk)];
+    for (int i = 0; i < CF::TM; ++i) av[i] = As[sw_a<CF>(simt_row<CF>(ty, i), kk)];
 #pragma unroll
     for (int c = 0; c < CF::TN / 2; ++c) {
-      const double2 v = *reinterpret_cast<const double2*>(Bs + sw_b(kk, tx, c));
+      const double2 v = *reinterpret_cast<const double2*>(Bs + sw_b<CF>(kk, tx, c));
       bv[2 * c] = v.x;
       bv[2 * c + 1] = v.y;
     }
@@ -141,8 +150,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
     for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
       for (int j = 0; j < CF::TN; ++j) {  // the update of P:122-132, every op separately rounded
-        const double x = dmul(av[i], bv[j]);
-        double e = dadd(err[i][j], x);
+        // (FUSED, NEXT-3 / reading R22: err = fma(a, b, err))
+        double e = FUSED ? __fma_rn(av[i], bv[j], err[i][j]) : dadd(err[i][j], dmul(av[i], bv[j]));
         const double t = dadd(sum[i][j], e);
         e = dadd(dsub(sum[i][j], t), e);
         sum[i][j] = t;
@@ -155,10 +164,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
     const int s = pp.acquire(a, kt);
     const double* As = pp.As_base + s * LY::A_TILE;
     const double* Bs = pp.Bs_base + s * LY::B_TILE;
-    const int64_t k0 = int64_t(kt) * 16;
-    if (k0 + 16 <= a.P) {
+    const int64_t k0 = int64_t(kt) * CF::BK;
+    if (k0 + CF::BK <= a.P) {
 #pragma unroll 4
-      for (int kk = 0; kk < 16; ++kk) step(As, Bs, kk);
+      for (int kk = 0; kk < CF::BK; ++kk) step(As, Bs, kk);
     } else {
       const int kmax = int(a.P - k0);  // stop exactly at P
       for (int kk = 0; kk < kmax; ++kk) step(As, Bs, kk);
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
   int64_t m0, n0;
   simt_tile_coords(a.N, a.M, CF::BM, CF::BN, m0, n0);
   SimtPipe<CF> pp;
-  pp.init(w_raw, int(m0), int(n0), int(cdiv(a.P, 16)));  // P even: 2 gamma = P
+  pp.init(w_raw, int(m0), int(n0), int(cdiv(a.P, CF::BK)));  // P even: 2 gamma = P
   pp.start(a);
 
   double acc[TM][TN];
@@ -209,18 +218,18 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
     // a zero-filled pair past P adds (0+0)(0+0) = +0 to acc, which leaves acc unchanged
     // (acc starts at +0 and can never become -0), so the last tile needs no guard
 #pragma unroll 2
-    for (int jp = 0; jp < 8; ++jp) {
+    for (int jp = 0; jp < CF::BK / 2; ++jp) {
       double a0[TM], a1[TM], b0[TN], b1[TN];
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const double2 v = *reinterpret_cast<const double2*>(As + sw_a(simt_row<CF>(ty, i), 2 * jp));
+        const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
         a0[i] = v.x;
         a1[i] = v.y;
       }
 #pragma unroll
       for (int c = 0; c < TN / 2; ++c) {
-        const double2 u = *reinterpret_cast<const double2*>(Bs + sw_b(2 * jp, tx, c));
-        const double2 w = *reinterpret_cast<const double2*>(Bs + sw_b(2 * jp + 1, tx, c));
+        const double2 u = *reinterpret_cast<const double2*>(Bs + sw_b<CF>(2 * jp, tx, c));
+        const double2 w = *reinterpret_cast<const double2*>(Bs + sw_b<CF>(2 * jp + 1, tx, c));
         b0[2 * c] = u.x;
         b0[2 * c + 1] = u.y;
         b1[2 * c] = w.x;
@@ -281,10 +290,10 @@ inline bool simt_tma_args(SimtTmaArgs& args, const double* A, const double* B, d
   args.P = P;
   args.M = M;
   return tma_encode_2d(&args.mapA, A, N, P, P, CF::BM, 16, true) &&
-         tma_encode_2d(&args.mapB, B, P, M, M, 16, 16, true);
+         tma_encode_2d(&args.mapB, B, P, M, M, CF::BK, 16, true);
 }
 
-template <class CF>
+template <class CF, bool FUSED = false>
 inline cudaError_t launch_kahan_tma(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                                     cudaStream_t st) {
   using LY = SimtTmaLayout<CF>;
@@ -292,8 +301,8 @@ inline cudaError_t launch_kahan_tma(const double* A, const double* B, double* C,
   if (!simt_tma_args<CF>(args, A, B, C, N, P, M)) return cudaErrorInvalidValue;
   const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
   const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
-  return cv ? launch_simt_tma_t_<kahan_tma_kernel<CF, 2>, CF::THREADS, LY::SMEM>(args, grid, st)
-            : launch_simt_tma_t_<kahan_tma_kernel<CF, 1>, CF::THREADS, LY::SMEM>(args, grid, st);
+  return cv ? launch_simt_tma_t_<kahan_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<kahan_tma_kernel<CF, 1, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st);
 }
 
 template <class CF, bool FUSED>

@@ -42,9 +42,9 @@ def expected(kernel: str):
     half = n3 // 2
     if kernel.startswith("dgemm"):
         return None  # batched Strassen leaves share the kernel; see the DMMA ratio column
-    if kernel.startswith("kahan_gemm_kernel") and kernel.rstrip(">").endswith("1"):
+    if kernel.startswith(("kahan_gemm_kernel", "kahan_tma_kernel")) and kernel.rstrip(">").endswith("1"):
         return {"dadd": 3 * n3, "dmul": 0, "dfma": n3, "dmma": 0}
-    if kernel.startswith("kahan_gemm_kernel"):
+    if kernel.startswith(("kahan_gemm_kernel", "kahan_tma_kernel")):
         return {"dadd": 4 * n3, "dmul": n3, "dfma": 0, "dmma": 0}
     if kernel.startswith("winograd_tma_kernel") and kernel.rstrip(">").endswith("1"):
         return {"dadd": 2 * half + 2 * n2, "dmul": 0, "dfma": half, "dmma": 0}

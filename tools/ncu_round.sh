@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 echo "launch list rc=$?"
 for M in naive kahan winograd; do
   QB="python tools/quick_bench.py --methods $M --reps 1"
-  case $M in naive) K=dgemm_tma;; kahan) K=kahan_gemm;; winograd) K=winograd_tma_kernel;; esac
+  case $M in naive) K=dgemm_tma;; kahan) K=kahan_tma_kernel;; winograd) K=winograd_tma_kernel;; esac
   $QB > $OUT/plain_qb_$M.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o $OUT/full_$M $QB > $OUT/ncu_full_$M.log 2>&1
   echo "full $M rc=$?"

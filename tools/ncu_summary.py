@@ -22,7 +22,7 @@ def family(name: str) -> str:
         return "line_kernel<0> (norm_inf)"
     if "line_kernel<1" in name or "line_kernel<2" in name:
         return "line_kernel<1> (winograd y/z)"
-    for k in ("dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
+    for k in ("dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_tma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
               "winograd_kernel",
               "strassen_form_kernel", "strassen_combine_kernel", "norm_inf_kernel", "scale_copy_kernel",
               "lambda_kernel"):

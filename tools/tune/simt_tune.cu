@@ -144,16 +144,11 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB, BK>
-  kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("64x64_t4x8_s2_2cta_bk32", c, true);
-  kahan<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
-  kahan<SimtCfg<32, 64, 2, 8, 3, 2>>("32x64_t2x8_s3_2cta", c, false);
-  kahan<SimtCfg<64, 32, 4, 4, 3, 3>>("64x32_t4x4_s3_3cta", c, false);
-  kahan<SimtCfg<32, 32, 2, 4, 3, 4>>("32x32_t2x4_s3_4cta", c, false);
-  kahan<SimtCfg<32, 64, 4, 4, 3, 4>>("32x64_t4x4_s3_4cta", c, false);
-  wino<SimtCfg<64, 64, 4, 8, 3, 2>>("64x64_t4x8_s3_2cta", c, true);
-  wino<SimtCfg<32, 64, 4, 8, 3, 3>>("32x64_t4x8_s3_3cta", c, false);
-  wino<SimtCfg<32, 64, 2, 8, 3, 3>>("32x64_t2x8_s3_3cta", c, false);
-  wino<SimtCfg<64, 32, 4, 4, 3, 4>>("64x32_t4x4_s3_4cta", c, false);
-  wino<SimtCfg<32, 32, 2, 4, 3, 4>>("32x32_t2x4_s3_4cta", c, false);
+  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
+  wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_s4_bk16", c);
+  wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_bk32", c);
+  wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_s4_bk16_again", c);
+  kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_bk32", c);
   return 0;
 }
