@@ -31,10 +31,10 @@ struct GemmTmaArgs {
 
 template <class CF>
 struct TmaLayout {
-  static constexpr int A_TILE = CF::BM * 16, B_TILE = 16 * CF::BN;  // doubles
+  static constexpr int A_TILE = CF::BM * CF::BK, B_TILE = CF::BK * CF::BN;  // doubles
   static constexpr unsigned STAGE_BYTES = unsigned(A_TILE + B_TILE) * 8u;
   static constexpr size_t SMEM = 1024 + size_t(CF::STAGES) * STAGE_BYTES + 2 * CF::STAGES * 8;
-  static_assert(CF::BK == 16, "one 128-byte swizzle row of k per tile row");
+  static_assert(CF::BK == 16 || CF::BK == 32, "one or two 128-byte swizzle rows of k per tile row");
   static_assert(CF::WTN % 16 == 0, "a warp covers whole 16-column B boxes");
 };
 
@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
   const int gsize = min(tiles_m - first_m, CF::GROUP_M);
   const int in_group = tile - group * CF::GROUP_M * tiles_n;
   const int m0 = (first_m + in_group % gsize) * BM, n0 = (in_group / gsize) * BN;
-  const int KT = int(cdiv(pr.P, 16));
+  constexpr int BK = CF::BK;
+  const int KT = int(cdiv(pr.P, BK));
 
   if (tid == 0) {
     tma_prefetch_desc(&args.mapA);
@@ -92,10 +93,12 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
 
   auto issue = [&](int kt, int s) {  // thread 0 only
     mbar_arrive_expect_tx(full + s, LY::STAGE_BYTES);
-    tma_load_3d(As_base + s * LY::A_TILE, &args.mapA, kt * 16, m0, int(bidx), full + s);
 #pragma unroll
-    for (int b = 0; b < BN / 16; ++b)
-      tma_load_3d(Bs_base + s * LY::B_TILE + b * 256, &args.mapB, n0 + 16 * b, kt * 16, int(bidx), full + s);
+    for (int h = 0; h < BK / 16; ++h)  // A: [BM rows][16 k] boxes
+      tma_load_3d(As_base + s * LY::A_TILE + h * (BM * 16), &args.mapA, kt * BK + 16 * h, m0, int(bidx), full + s);
+#pragma unroll
+    for (int b = 0; b < BN / 16; ++b)  // B: [BK k][16 columns] boxes
+      tma_load_3d(Bs_base + s * LY::B_TILE + b * (BK * 16), &args.mapB, n0 + 16 * b, kt * BK, int(bidx), full + s);
   };
   if (tid == 0)
     for (int s = 0; s < STAGES && s < KT; ++s) issue(s, s);
@@ -148,9 +151,9 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
     const double* As = As_base + s * LY::A_TILE;
     const double* Bs = Bs_base + s * LY::B_TILE;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
+    for (int ks = 0; ks < BK / 4; ++ks) {
       const int k = ks * 4 + t;
-      const int a_off = ((((k >> 1) ^ rho)) << 1) + (k & 1);
+      const int a_off = (k >> 4) * (BM * 16) + (((((k & 15) >> 1) ^ rho)) << 1) + (k & 1);
       const int k8 = k & 7;
       double af[MI], bf[NJ];
 #pragma unroll
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_BLOCKS) dgemm_tma_kernel(
 #pragma unroll
       for (int nj = 0; nj < NJ; ++nj) {
         const int sg = (nj & 1) ? sig1 : sig0;
-        bf[nj] = Bs[(b_box0 + (nj >> 1)) * 256 + k * 16 + ((((sg >> 1) ^ k8)) << 1) + (sg & 1)];
+        bf[nj] = Bs[(b_box0 + (nj >> 1)) * (BK * 16) + k * 16 + ((((sg >> 1) ^ k8)) << 1) + (sg & 1)];
       }
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
@@ -212,7 +215,7 @@ inline cudaError_t launch_dgemm_tma(const GemmProblem& pr, cudaStream_t st) {
   GemmTmaArgs args;
   args.pr = pr;
   if (!tma_encode_3d(&args.mapA, pr.A, pr.N, pr.P, pr.lda, pr.batch, pr.sA, CF::BM) ||
-      !tma_encode_3d(&args.mapB, pr.B, pr.P, pr.M, pr.ldb, pr.batch, pr.sB, 16))
+      !tma_encode_3d(&args.mapB, pr.B, pr.P, pr.M, pr.ldb, pr.batch, pr.sB, CF::BK))
     return cudaErrorInvalidValue;
   const bool cv = (reinterpret_cast<uintptr_t>(pr.C) & 15) == 0 && pr.ldc % 2 == 0 && (pr.batch == 1 || pr.sC % 2 == 0);
   const int64_t tiles = cdiv(pr.N, CF::BM) * cdiv(pr.M, CF::BN);
@@ -230,10 +233,11 @@ inline cudaError_t launch_dgemm_tma(const GemmProblem& pr, cudaStream_t st) {
 #ifndef GEMM_TMA_GROUP_M
 #define GEMM_TMA_GROUP_M 8
 #endif
-// the production configuration of the TMA path: 64 x 64 tiles, 4 warps of 32 x 32, 4 stages,
-// 3 CTAs (12 warps) per SM -- 36.1 TF at 8192^3, 34.0 at 2048^3, 27.5 at 1024^3 on B200
-// (tools/tune/gemm_tune.cu, profiles/r01/gemm_tune_tma.jsonl; cuBLAS DGEMM: 35.5 at 8192^3)
-using GemmTma = GemmCfg<64, 64, 2, 2, 4, 3, 16, GEMM_TMA_GROUP_M>;
+// the production configuration of the TMA path: 64 x 64 x 32 tiles, 4 warps of 32 x 32, double
+// buffered, 3 CTAs (12 warps) per SM -- 36.3 TF at 8192^3, 34.4 at 2048^3 on B200 (16-deep tiles,
+// 4 stages: 36.26 / 33.8; tools/tune/gemm_tune.cu, profiles/r01/gemm_tune_tma.jsonl,
+// gemm_tune_bk32.jsonl; cuBLAS DGEMM: 35.5 at 8192^3)
+using GemmTma = GemmCfg<64, 64, 2, 2, 2, 3, 32, GEMM_TMA_GROUP_M>;
 // fewer than two waves of 64 x 64 tiles (e.g. 1024^3): 64 x 32 tiles, 2 warps of 32 x 32, 6 CTAs
 // per SM -- 28.2 vs 26.6 TF at 1024^3 (profiles/r01/gemm_tune_small.jsonl)
 using GemmTmaSmall = GemmCfg<64, 32, 2, 1, 4, 6, 16, GEMM_TMA_GROUP_M>;

@@ -120,11 +120,10 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
-  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_w2x2_s4_3cta", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<64, 32, 2, 1, 4, 6>, true>("tma_64x32_w2x1_s4_6cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<32, 64, 1, 2, 4, 6>, true>("tma_32x64_w1x2_s4_6cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<32, 32, 1, 1, 4, 10>, true>("tma_32x32_w1x1_s4_10cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 32, 2, 1, 6, 4>, true>("tma_64x32_w2x1_s6_4cta", A, B, C, R, n, reps, bad);
-  run<GemmCfg<32, 64, 2, 2, 4, 6>, true>("tma_32x64_w2x2_s4_6cta", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_s4_3cta_bk16", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 2, 3, 32>, true>("tma_64x64_s2_3cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 3, 3, 32>, true>("tma_64x64_s3_3cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 3, 2, 32>, true>("tma_64x64_s3_2cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_s4_3cta_bk16_again", A, B, C, R, n, reps, bad);
   return 0;
 }
