@@ -48,5 +48,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB_PATH
 
 
+def build_tools(verbose: bool = False) -> str:
+    """tools/mmtest: the paper's test program as a plain C client of the C ABI (no Python)."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tools", "mmtest.c")
+    out = os.path.join(root, "tools", "mmtest")
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src), os.path.getmtime(LIB_PATH)):
+        return out
+    cuda = os.path.dirname(os.path.dirname(nvcc())) if os.path.sep in nvcc() else "/usr/local/cuda"
+    cmd = ["gcc", "-O2", "-std=c99", "-Wall", "-I", INCLUDE, "-I", os.path.join(cuda, "include"), src,
+           "-L", HERE, "-lmm_b200", "-L", os.path.join(cuda, "lib64"), "-lcudart", "-lm",
+           "-Wl,-rpath," + HERE, "-Wl,-rpath,$ORIGIN/../paper_1106_1347_b200", "-o", out]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
