@@ -24,7 +24,9 @@
  *    MM_ERR_CUDA: a launch or CUDA runtime call failed (device faults surface at the
  *    caller's next synchronisation).  On error nothing is enqueued unless MM_ERR_CUDA.
  *  - Arithmetic is IEEE binary64 round-to-nearest-even throughout; DESIGN.md lists, per
- *    method, which oracle function each kernel reproduces bit for bit.
+ *    method, which oracle function each kernel reproduces bit for bit.  The paper defines the
+ *    methods on finite inputs only; with NaN/Inf operands the IEEE propagation of each operation
+ *    applies (norm_inf then returns a NaN if any row sum is NaN), and no result is guaranteed.
  */
 #ifndef MM_B200_H
 #define MM_B200_H
