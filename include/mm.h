@@ -22,7 +22,8 @@
  *    MM_ERR_WORKSPACE: ws_bytes < mm_workspace_size(...).  MM_ERR_UNSUPPORTED: the current
  *    device is not compute capability 10.0 (sm_100a) -- there is no fallback of any kind.
  *    MM_ERR_CUDA: a launch or CUDA runtime call failed (device faults surface at the
- *    caller's next synchronisation).  On error nothing is enqueued unless MM_ERR_CUDA.
+ *    caller's next synchronisation).  MM_ERR_NCCL: the multi-GPU layer could not load NCCL or a
+ *    collective failed.  On error nothing is enqueued unless MM_ERR_CUDA / MM_ERR_NCCL.
  *  - Arithmetic is IEEE binary64 round-to-nearest-even throughout; DESIGN.md lists, per
  *    method, which oracle function each kernel reproduces bit for bit.  The paper defines the
  *    methods on finite inputs only; with NaN/Inf operands the IEEE propagation of each operation
@@ -43,6 +44,7 @@ typedef enum {
   MM_ERR_ALIAS = -2,
   MM_ERR_WORKSPACE = -3,
   MM_ERR_CUDA = -4,
+  MM_ERR_NCCL = -5,
   MM_ERR_UNSUPPORTED = -6
 } mm_status;
 
@@ -188,6 +190,38 @@ int mm_winograd_fused(const double* A, const double* B, double* C, int64_t N, in
                       void* workspace, size_t ws_bytes, void* stream);
 int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                              void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
+
+/*
+ * Multi-GPU row-block layer (BASELINE.json north_star: "C is partitioned by
+ * row blocks of A with B broadcast over NVLink through NCCL").  One process per GPU.  NCCL is
+ * loaded at run time (the soname libnccl.so.2 if resident -- e.g. after PyTorch initialised NCCL --
+ * else the path in the environment variable MM_NCCL_LIBRARY); without it these return MM_ERR_NCCL
+ * and the rest of the library is unaffected.  One communicator per process.
+ *
+ * mm_dist_get_unique_id -- rank 0 creates the 128-byte NCCL id (HOST buffer) that every rank
+ *   passes to mm_dist_init (distribute it out of band, e.g. torch.distributed).
+ * mm_dist_init -- join the communicator as `rank` of `world` on CUDA device `device` (made
+ *   current).  MM_ERR_ARG if already initialised or arguments are out of range.
+ * mm_dist_gemm -- C_shard = A_shard B for this rank's N_local rows (N_local >= 0; a rank without
+ *   rows still takes part in the collectives).  B: DEVICE buffer P x M on every rank; the root's
+ *   content is broadcast into it in place inside the call.  method: an mm_method id.  For
+ *   MM_NAIVE with panels > 1, B travels as `panels` (<= 64) row panels on the layer's own stream
+ *   and the product accumulates panel by panel (mm_naive_ex), each panel's multiply waiting only
+ *   for its own transfer -- bitwise the one-shot product.  WinogradScaled uses the global
+ *   ||A||_inf (max-all-reduce of the row blocks' norms) and the local ||B||_inf, so lambda equals
+ *   the one-GPU lambda.  Classical, Kahan and both Winograds are bitwise the rows of the one-GPU
+ *   product; Strassen recurses on the shard (within its tolerance).  workspace: DEVICE, >=
+ *   mm_dist_workspace_size(...).  Stream-ordered and asynchronous like the other entry points;
+ *   the current device must be the one given to mm_dist_init.
+ * mm_dist_finalize -- destroy the communicator and the layer's stream and events.
+ */
+int mm_dist_get_unique_id(void* id_out);
+int mm_dist_init(int32_t rank, int32_t world, const void* unique_id, int32_t device);
+size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M, int32_t levels);
+int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, int64_t N_local, int64_t P,
+                 int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
+                 void* stream);
+int mm_dist_finalize(void);
 
 /*
  * mm_launch_count -- number of kernels this library has launched in this process (a

@@ -43,7 +43,8 @@ METHODS = {
 EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winograd", "mm_winograd_scaled",
            "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
            "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
-           "mm_winograd_scaled_fused", "mm_naive_ex")
+           "mm_winograd_scaled_fused", "mm_naive_ex", "mm_dist_get_unique_id", "mm_dist_init",
+           "mm_dist_workspace_size", "mm_dist_gemm", "mm_dist_finalize")
 
 
 class MMError(RuntimeError):
@@ -68,6 +69,11 @@ def lib() -> ctypes.CDLL:
         for n in ("mm_naive", "mm_kahan", "mm_kahan_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp]
         L.mm_naive_ex.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, i64, i32, vp]
+        L.mm_dist_get_unique_id.argtypes = [ctypes.c_char_p]
+        L.mm_dist_init.argtypes = [i32, i32, ctypes.c_char_p, i32]
+        L.mm_dist_workspace_size.argtypes = [ctypes.c_int, i64, i64, i64, i32]
+        L.mm_dist_workspace_size.restype = sz
+        L.mm_dist_gemm.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64, i32, i32, i32, vp, sz, vp]
         for n in ("mm_winograd", "mm_winograd_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
         for n in ("mm_winograd_scaled", "mm_winograd_scaled_fused"):

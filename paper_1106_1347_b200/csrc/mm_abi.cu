@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "dist_nccl.cuh"
 #include "gemm_tma.cuh"
 #include "kahan.cuh"
 #include "norm_lambda.cuh"
@@ -92,6 +93,7 @@ const char* mm_status_string(int status) {
     case MM_ERR_WORKSPACE: return "workspace too small (see mm_workspace_size)";
     case MM_ERR_CUDA: return "CUDA launch or runtime error";
     case MM_ERR_UNSUPPORTED: return "current device is not sm_100 (B200); no fallback exists";
+    case MM_ERR_NCCL: return "NCCL unavailable or an NCCL call failed (multi-GPU layer)";
     default: return "unknown status";
   }
 }
@@ -281,6 +283,117 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
       return mm_winograd_scaled_fused(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
     default: return MM_ERR_ARG;
   }
+}
+
+// ---------------------------------------------------------------- multi-GPU row-block layer (K9)
+int mm_dist_get_unique_id(void* id_out) {
+  if (!id_out) return MM_ERR_ARG;
+  mmk::NcclApi* api = mmk::nccl_api();
+  if (!api) return MM_ERR_NCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return MM_ERR_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return MM_OK;
+}
+
+int mm_dist_init(int32_t rank, int32_t world, const void* unique_id, int32_t device) {
+  mmk::DistState& ds = mmk::dist_state();
+  if (!unique_id || world < 1 || rank < 0 || rank >= world || device < 0 || ds.comm) return MM_ERR_ARG;
+  mmk::NcclApi* api = mmk::nccl_api();
+  if (!api) return MM_ERR_NCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return cuda_status(cudaErrorInvalidDevice);
+  int rc = check_device(nullptr);
+  if (rc) return rc;
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  if (api->CommInitRank(&ds.comm, world, id, rank) != ncclSuccess) {
+    ds.comm = nullptr;
+    return MM_ERR_NCCL;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&ds.comm_stream, cudaStreamNonBlocking);
+  for (int i = 0; e == cudaSuccess && i < mmk::DistState::kMaxPanels; ++i)
+    e = cudaEventCreateWithFlags(&ds.panel_ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ds.start_ev, cudaEventDisableTiming);
+  ds.rank = rank;
+  ds.world = world;
+  ds.device = device;
+  return cuda_status(e);
+}
+
+int mm_dist_finalize(void) {
+  mmk::DistState& ds = mmk::dist_state();
+  if (!ds.comm) return MM_ERR_ARG;
+  mmk::NcclApi* api = mmk::nccl_api();
+  const ncclResult_t r = api->CommDestroy(ds.comm);
+  if (ds.comm_stream) cudaStreamDestroy(ds.comm_stream);
+  for (int i = 0; i < mmk::DistState::kMaxPanels; ++i)
+    if (ds.panel_ev[i]) cudaEventDestroy(ds.panel_ev[i]);
+  if (ds.start_ev) cudaEventDestroy(ds.start_ev);
+  ds = mmk::DistState();
+  return r == ncclSuccess ? MM_OK : MM_ERR_NCCL;
+}
+
+constexpr size_t kDistHeader = 256;  // the two norms of the distributed WinogradScaled
+
+size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M, int32_t levels) {
+  const int64_t n = N_local > 0 ? N_local : 1;
+  if (method == MM_WINOGRAD_SCALED || method == MM_WINOGRAD_SCALED_FUSED)
+    return kDistHeader + mm_workspace_size(method, n, P, M, levels);
+  return mm_workspace_size(method, n, P, M, levels);
+}
+
+int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, int64_t N_local, int64_t P,
+                 int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
+                 void* stream) {
+  mmk::DistState& ds = mmk::dist_state();
+  if (!ds.comm || !B || P < 1 || M < 1 || N_local < 0 || root < 0 || root >= ds.world) return MM_ERR_ARG;
+  if (N_local > 0 && (!A_shard || !C_shard)) return MM_ERR_ARG;
+  if (!mul_ok(P, M) || (N_local > 0 && (!mul_ok(N_local, P) || !mul_ok(N_local, M)))) return MM_ERR_ARG;
+  if (ws_bytes < mm_dist_workspace_size(method, N_local, P, M, levels)) return MM_ERR_WORKSPACE;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != ds.device) return MM_ERR_ARG;
+  mmk::NcclApi* api = mmk::nccl_api();
+  cudaStream_t st = S(stream);
+  const size_t count = size_t(P) * size_t(M);
+  if (method == MM_NAIVE && panels > 1) {
+    // NEXT-4: panel i of B crosses NVLink on the comm stream while panel i-1 is multiplied
+    int64_t bounds[mmk::DistState::kMaxPanels + 1];
+    const int np = mmk::dist_panel_bounds(P, panels, bounds);
+    cudaError_t e = cudaEventRecord(ds.start_ev, st);  // B may be rewritten once prior work on st is done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds.comm_stream, ds.start_ev, 0);
+    if (e != cudaSuccess) return cuda_status(e);
+    for (int i = 0; i < np; ++i) {
+      double* Bp = B + bounds[i] * M;
+      if (api->Broadcast(Bp, Bp, size_t(bounds[i + 1] - bounds[i]) * size_t(M), ncclFloat64, root, ds.comm,
+                         ds.comm_stream) != ncclSuccess)
+        return MM_ERR_NCCL;
+      if ((e = cudaEventRecord(ds.panel_ev[i], ds.comm_stream)) != cudaSuccess) return cuda_status(e);
+    }
+    for (int i = 0; i < np; ++i) {
+      if ((e = cudaStreamWaitEvent(st, ds.panel_ev[i], 0)) != cudaSuccess) return cuda_status(e);
+      if (N_local == 0) continue;
+      const int rc = mm_naive_ex(A_shard + bounds[i], P, B + bounds[i] * M, M, C_shard, M, N_local,
+                                 bounds[i + 1] - bounds[i], M, i > 0 ? 1 : 0, stream);
+      if (rc) return rc;
+    }
+    return MM_OK;
+  }
+  if (api->Broadcast(B, B, count, ncclFloat64, root, ds.comm, st) != ncclSuccess) return MM_ERR_NCCL;
+  if (method == MM_WINOGRAD_SCALED || method == MM_WINOGRAD_SCALED_FUSED) {
+    // global ||A|| = max over the row blocks (order-free, exact); ||B|| is local (B replicated)
+    auto* norms = static_cast<unsigned long long*>(workspace);
+    cudaError_t e = N_local > 0 ? mmk::launch_norm_inf(A_shard, N_local, P, norms, st)
+                                : cudaMemsetAsync(norms, 0, sizeof(double), st);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (api->AllReduce(norms, norms, 1, ncclFloat64, ncclMax, ds.comm, st) != ncclSuccess) return MM_ERR_NCCL;
+    if ((e = mmk::launch_norm_inf(B, P, M, norms + 1, st)) != cudaSuccess) return cuda_status(e);
+    if (N_local == 0) return MM_OK;
+    return winograd_scaled_common(method == MM_WINOGRAD_SCALED_FUSED, A_shard, B, C_shard, N_local, P, M,
+                                  reinterpret_cast<const double*>(norms), static_cast<char*>(workspace) + kDistHeader,
+                                  ws_bytes - kDistHeader, nullptr, stream);
+  }
+  if (N_local == 0) return MM_OK;
+  return mm_gemm(method, A_shard, B, C_shard, N_local, P, M, levels, workspace, ws_bytes, nullptr, stream);
 }
 
 int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, void* stream) {

@@ -100,3 +100,64 @@ def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optio
     if A_local.shape[0] == 0:
         return torch.empty((0, B.shape[1]), dtype=B.dtype, device=B.device)
     return compute(method, A_local, B, out, levels, norms)
+
+
+class NativeComm:
+    """The C ABI's own multi-GPU layer (mm_dist_*: NCCL driven from libmm_b200.so, broadcast of B
+    and the panelised overlap on the library's streams).  torch.distributed only bootstraps it:
+    rank 0's 128-byte NCCL id reaches the other ranks through broadcast_object_list."""
+
+    def __init__(self, group=None):
+        import ctypes
+        import os
+
+        import paper_1106_1347_b200 as mm
+
+        if "MM_NCCL_LIBRARY" not in os.environ:
+            try:  # the NCCL PyTorch ships (used when the soname is not already resident)
+                import nvidia.nccl
+
+                os.environ["MM_NCCL_LIBRARY"] = os.path.join(nvidia.nccl.__path__[0], "lib", "libnccl.so.2")
+            except ImportError:
+                pass
+        self.mm = mm
+        self.L = mm.lib()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        buf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            mm._check(self.L.mm_dist_get_unique_id(buf), "mm_dist_get_unique_id")
+        obj = [buf.raw]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.device = torch.cuda.current_device()
+        mm._check(self.L.mm_dist_init(self.rank, self.world, obj[0], self.device), "mm_dist_init")
+        self._ws = None
+
+    def gemm(self, method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None,
+             root: int = 0, levels: int = 2, panels: int = 1, stream=None) -> torch.Tensor:
+        """C_local = A_local B through mm_dist_gemm (B: P x M on every rank, broadcast in place)."""
+        mm = self.mm
+        N, P = A_local.shape
+        M = B.shape[1]
+        for t in (A_local, B):
+            if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("A_local and B must be contiguous float64 CUDA tensors")
+        if B.shape[0] != P:
+            raise ValueError("inner dimensions differ")
+        if out is None:
+            out = torch.empty((N, M), dtype=torch.float64, device=B.device)
+        mid = mm.METHODS[method]
+        lv = levels if method in ("strassen", "strassen_winograd") else 0
+        nbytes = int(self.L.mm_dist_workspace_size(mid, N, P, M, lv))
+        if nbytes and (self._ws is None or self._ws.numel() < nbytes):
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=B.device)
+        ws_ptr = self._ws.data_ptr() if nbytes else None
+        s = stream if stream is not None else torch.cuda.current_stream(B.device)
+        mm._check(self.L.mm_dist_gemm(mid, A_local.data_ptr() if N else None, B.data_ptr(),
+                                      out.data_ptr() if N else None, N, P, M, root, lv, panels, ws_ptr, nbytes,
+                                      s.cuda_stream), f"mm_dist_gemm({method})")
+        return out
+
+    def close(self):
+        if self.L is not None:
+            self.mm._check(self.L.mm_dist_finalize(), "mm_dist_finalize")
+            self.L = None

@@ -93,3 +93,15 @@ def test_no_fallback_without_gpu(L):
         pytest.skip("has a GPU")
     # well-formed arguments on a machine without a B200: unsupported, nothing computed
     assert L.mm_naive(1 << 20, 1 << 24, 1 << 28, 16, 16, 16, None) == -6
+
+
+def test_dist_layer_host_errors():
+    """mm_dist_* before mm_dist_init: argument errors, no crash, no GPU needed."""
+    import paper_1106_1347_b200 as mm
+
+    L = mm.lib()
+    assert L.mm_dist_gemm(0, None, None, None, 1, 1, 1, 0, 0, 1, None, 0, None) == -1  # MM_ERR_ARG
+    assert L.mm_dist_finalize() == -1
+    assert L.mm_dist_init(0, 1, None, 0) == -1
+    assert L.mm_dist_workspace_size(3, 4, 5, 6, 0) >= L.mm_workspace_size(3, 4, 5, 6, 0) + 256
+    assert b"NCCL" in L.mm_status_string(-5)

@@ -2,7 +2,8 @@
 group on cuda:0, so the broadcast (plain and the NEXT-4 panelised async one, whose work.wait()
 makes the compute stream wait on NCCL's stream) and the max-all-reduce of ||A|| run through NCCL
 and the local products through the C ABI.  Every method's result must equal the single-GPU call
-bit for bit.  (Only one GPU is available to this test suite; world_size 2 is covered on gloo.)"""
+bit for bit, both through the torch.distributed driver and through the C ABI's own NCCL layer
+(mm_dist_*).  (Only one GPU is available to this test suite; world_size 2 is covered on gloo.)"""
 import os
 import socket
 import subprocess
@@ -35,6 +36,24 @@ SCRIPT = textwrap.dedent(r"""
             C = dist_gemm(m, dA, Bw, levels=2, panels=panels)
             torch.cuda.synchronize()
             assert torch.equal(C, ref), (m, panels)
+    # the C ABI's own layer (mm_dist_*): NCCL driven from libmm_b200.so
+    from paper_1106_1347_b200.dist import NativeComm
+    comm = NativeComm()
+    for m in ("naive", "kahan", "winograd", "winograd_scaled", "strassen", "strassen_winograd",
+              "kahan_fused", "winograd_fused", "winograd_scaled_fused"):
+        kw = {"levels": 2} if m.startswith("strassen") else {}
+        ref = getattr(mm, m)(dA, hB, **kw)
+        for panels in (1, 3, 8):
+            Bw = hB.clone()
+            C = comm.gemm(m, dA, Bw, levels=2, panels=panels)
+            torch.cuda.synchronize()
+            assert torch.equal(C, ref), ("native", m, panels)
+            assert torch.equal(Bw, hB)
+    # a rank without rows still takes part (the product is empty)
+    C0 = comm.gemm("winograd_scaled", dA[:0], hB.clone())
+    torch.cuda.synchronize()
+    assert C0.shape == (0, hB.shape[1])
+    comm.close()
     dist.destroy_process_group()
     print("nccl world-1 ok")
 """)
