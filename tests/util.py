@@ -1,6 +1,7 @@
 """Test helpers: device staging and oracle parallelism (no method arithmetic here)."""
 from __future__ import annotations
 
+import multiprocessing
 import os
 from concurrent.futures import ProcessPoolExecutor
 
@@ -40,7 +41,8 @@ def oracle_rows(name: str, A: np.ndarray, B: np.ndarray, lam: int = 0) -> np.nda
     if nw == 1 or A.shape[0] < 64:
         return _rows_job((name, A, B, lam))
     blocks = np.array_split(np.arange(A.shape[0]), nw)
-    with ProcessPoolExecutor(nw) as ex:
+    # forkserver: the test process has CUDA (and its threads) initialised; forking it is unsafe
+    with ProcessPoolExecutor(nw, mp_context=multiprocessing.get_context("forkserver")) as ex:
         parts = list(ex.map(_rows_job, [(name, np.ascontiguousarray(A[b]), B, lam) for b in blocks if len(b)]))
     return np.concatenate(parts, axis=0)
 

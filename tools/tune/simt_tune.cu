@@ -144,11 +144,11 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB, BK>
-  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
-  wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_s4_bk16", c);
-  wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_bk32", c);
-  wino_tma<SimtCfg<128, 64, 8, 8, 4, 2>>("tma_128x64_s4_bk16_again", c);
   kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
-  kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_bk32", c);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_2cta_bk32", c);
+  kahan_tma<SimtCfg<64, 64, 4, 8, 2, 3, 32>>("tma_64x64_s2_3cta_bk32", c);
+  wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
+  wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_2cta_bk32", c);
+  wino_tma<SimtCfg<64, 64, 8, 8, 2, 3, 32>>("tma_64x64_t8x8_s2_3cta_bk32", c);
   return 0;
 }
