@@ -61,6 +61,8 @@ def parse_args():
                     help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="N > 1 collectives (gloo only to exercise the multi-rank path on fewer GPUs)")
+    ap.add_argument("--e2e-blocks", type=int, default=8,
+                    help="e2e: k-panels / row blocks the host<->device copies are pipelined in")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -402,7 +404,7 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
 
     def step():
         if world == 1:
-            mm.matmul_methods(hA, hB, order, levels=args.levels, outs=houts)
+            mm.matmul_methods(hA, hB, order, levels=args.levels, outs=houts, row_blocks=args.e2e_blocks)
             return
         # N > 1: each rank's rows of A (and B on the root) copied once per step; every product
         # broadcasts B inside dist_gemm and its C rows come back to the host
