@@ -396,3 +396,15 @@ def test_matmul_methods_bitwise():
         for m in order:
             ref = host(run(m, dA, dB, 1))
             assert np.array_equal(outs[m].numpy(), ref), (order, m)
+
+
+@pytest.mark.parametrize("method", ["strassen", "strassen_winograd"])
+def test_c2_paper_plan_bitwise(method, c2_ops):
+    """The paper's own padding plan (1024 -> k = 6, m = 17, Y = 1088; 7^6 leaves of order 17)
+    at c2, bitwise against the oracle's recursion with the same plan and the DMMA base (R19)."""
+    A, B = c2_ops[0]
+    C = host(run(method, dev(A), dev(B), -1))
+    ref = oracle.strassen(0 if method == "strassen" else 1, A, B, base=oracle.BASE_FMA)
+    assert np.array_equal(C, ref)
+    lit = oracle_rows("naive_standard", A, B)
+    assert norm_rows_err(C, lit) <= tol_for(method) * oracle.norm_inf(A) * oracle.norm_inf(B)
