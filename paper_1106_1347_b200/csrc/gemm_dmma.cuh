@@ -249,7 +249,12 @@ inline cudaError_t launch_dgemm_cfg(const GemmProblem& pr, cudaStream_t st) {
 // aligned (odd P) the 64 x 64 / 4-CTA configuration is faster at every size measured (c3
 // 4096 x 1001 x 3000: 0.85 vs 1.06 ms; 8192 x 8191 x 8192: 30.9 vs 27.9 TF;
 // profiles/r01/gemm_tune_oddP.jsonl)
+// tiny batched problems with an odd pitch (the paper plan's order-17 leaves): one warp per
+// 32 x 32 tile
+using GemmTiny = GemmCfg<32, 32, 1, 1, 4, 8>;
+
 inline cudaError_t launch_dgemm_cpasync(const GemmProblem& pr, cudaStream_t st, int sms = 148) {
+  if (pr.N <= 32 && pr.M <= 32 && pr.batch > 1) return launch_dgemm_cfg<GemmTiny>(pr, st);
   const bool a16 = (reinterpret_cast<uintptr_t>(pr.A) & 15) == 0 && pr.lda % 2 == 0 && (pr.batch == 1 || pr.sA % 2 == 0);
   const int64_t tiles = cdiv(pr.N, GemmDefault::BM) * cdiv(pr.M, GemmDefault::BN) * pr.batch;
   if (a16 && tiles >= 4 * int64_t(sms)) return launch_dgemm_cfg<GemmDefault>(pr, st);

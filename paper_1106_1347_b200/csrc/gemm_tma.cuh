@@ -244,8 +244,14 @@ using GemmTmaSmall = GemmCfg<64, 32, 2, 1, 4, 6, 16, GEMM_TMA_GROUP_M>;
 
 // K1 entry: TMA-staged kernel when the operands allow a tensor map, else the cp.async kernel
 // (same k order, bitwise the same result)
+// tiny problems (each at most 32 x 32 outputs: the leaves of the paper's Strassen plan, orders
+// 17..32) batched by the thousand: one warp per 32 x 32 tile instead of a 64 x 64 CTA
+// that would leave three quarters of its DMMAs padding
+using GemmTmaTiny = GemmCfg<32, 32, 1, 1, 2, 8, 32, GEMM_TMA_GROUP_M>;
+
 inline cudaError_t launch_dgemm(const GemmProblem& pr, cudaStream_t st, int sms = 148) {
   if (gemm_tma_ok(pr)) {
+    if (pr.N <= 32 && pr.M <= 32 && pr.batch > 1) return launch_dgemm_tma<GemmTmaTiny>(pr, st);
     const int64_t tiles = cdiv(pr.N, GemmTma::BM) * cdiv(pr.M, GemmTma::BN) * pr.batch;
     if (tiles < 2 * 3 * int64_t(sms)) return launch_dgemm_tma<GemmTmaSmall>(pr, st);
     return launch_dgemm_tma<GemmTma>(pr, st);
