@@ -9,3 +9,7 @@ tail -3 gpurun_out/pytest_gpu.txt
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 cat gpurun_out/bench.json
 [ "${NO_NCU:-0}" = 1 ] || timeout 1200 bash tools/ncu_round.sh
+# the paper's section-3 experiment on the GPU (Python and plain-C clients) and the per-config table
+timeout 900 python tools/paper_experiment.py --sizes 200,400,800,1600,3200,4096,8192 --json gpurun_out/paper_experiment.jsonl > gpurun_out/paper_experiment.txt 2>&1; echo paper rc=$?
+./tools/mmtest -O 800 -R 10 > gpurun_out/mmtest.txt 2>&1; echo mmtest rc=$?
+timeout 900 python tools/table_bench.py --reps 5 > gpurun_out/table.jsonl 2> gpurun_out/table.err; echo table rc=$?
