@@ -353,7 +353,8 @@ def run_mine(args):
                                           "frac": None, "traffic": None, "kernel": dom})
     roofline["share_of_step"] = round(per_m[dom] / ms, 4)
     roofline["peak_source"] = ("derived: 148 SMs x 64 FP64 lanes x 1.965 GHz (MEASURED_PEAKS.json has no FP64 "
-                               "entry; probe P2 measured DMMA 37.0 TF, DFMA 34.0 TF)")
+                               "entry; probes measured DMMA 37.0 TF and DADD 18.48 / DMUL 18.44 T op/s, "
+                               "profiles/r01_probe)")
 
     # ---- e2e: the user-level call on pinned host buffers, copies inside the timed region
     e2e = None
