@@ -173,8 +173,9 @@ def _gemm(method: int, name: str, A, B, out=None, levels: int = 0, stream=None, 
     ws_ptr, ws_len = _workspace(ws_bytes, A.device)
     lam = ctypes.c_int32(0)
     st = _stream_handle(stream, A.device)
-    rc = L.mm_gemm(method, A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, levels, ws_ptr, ws_len,
-                   ctypes.byref(lam) if want_lambda else None, st)
+    with torch.cuda.device(A.device):  # the library launches on the current device
+        rc = L.mm_gemm(method, A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, levels, ws_ptr, ws_len,
+                       ctypes.byref(lam) if want_lambda else None, st)
     _check(rc, name)
     if want_lambda:
         return out, int(lam.value)
@@ -198,8 +199,12 @@ def naive_panel(A, B, C, *, accumulate: bool, stream=None):
     if B.shape[0] != K or C.shape != (N, B.shape[1]):
         raise ValueError(f"shape mismatch: {tuple(A.shape)} x {tuple(B.shape)} -> {tuple(C.shape)}")
     M = B.shape[1]
-    _check(lib().mm_naive_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), N, K,
-                             M, 1 if accumulate else 0, _stream_handle(stream, A.device)), "mm_naive_ex")
+    if not (A.device == B.device == C.device):
+        raise ValueError("A, B, C must be on one device")
+    with torch.cuda.device(A.device):
+        rc = lib().mm_naive_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), N,
+                               K, M, 1 if accumulate else 0, _stream_handle(stream, A.device))
+    _check(rc, "mm_naive_ex")
     return C
 
 
@@ -235,9 +240,10 @@ def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False,
     L = lib()
     ws_ptr, ws_len = _workspace(int(L.mm_workspace_size(MM_WINOGRAD_SCALED, N, P, M, 0)), A.device)
     lam = ctypes.c_int32(0)
-    rc = L.mm_winograd_scaled_norms(A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, norms.data_ptr(), ws_ptr,
-                                    ws_len, ctypes.byref(lam) if return_lambda else None,
-                                    _stream_handle(stream, A.device))
+    with torch.cuda.device(A.device):
+        rc = L.mm_winograd_scaled_norms(A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, norms.data_ptr(), ws_ptr,
+                                        ws_len, ctypes.byref(lam) if return_lambda else None,
+                                        _stream_handle(stream, A.device))
     _check(rc, "mm_winograd_scaled_norms")
     return (out, int(lam.value)) if return_lambda else out
 
@@ -281,8 +287,9 @@ def norm_inf(X: torch.Tensor, *, out=None, stream=None) -> torch.Tensor:
         raise ValueError("X must be a contiguous float64 CUDA matrix")
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=X.device)
-    _check(lib().norm_inf(X.data_ptr(), X.shape[0], X.shape[1], out.data_ptr(), _stream_handle(stream, X.device)),
-           "norm_inf")
+    with torch.cuda.device(X.device):
+        rc = lib().norm_inf(X.data_ptr(), X.shape[0], X.shape[1], out.data_ptr(), _stream_handle(stream, X.device))
+    _check(rc, "norm_inf")
     return out
 
 
@@ -493,14 +500,15 @@ class GraphedProduct:
             _check(L.mm_gemm(mid, A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, lv, ws_ptr, ws_len, None,
                              stream.cuda_stream), f"mm_gemm({method})")
 
-        side = torch.cuda.Stream(A.device)
-        side.wait_stream(torch.cuda.current_stream(A.device))
-        with torch.cuda.stream(side):
-            call(side)  # warm-up outside capture: kernel attributes, occupancy queries, tensor maps
-        torch.cuda.current_stream(A.device).wait_stream(side)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            call(torch.cuda.current_stream(A.device))
+        with torch.cuda.device(A.device):  # the library launches on the current device
+            side = torch.cuda.Stream(A.device)
+            side.wait_stream(torch.cuda.current_stream(A.device))
+            with torch.cuda.stream(side):
+                call(side)  # warm-up outside capture: kernel attributes, occupancy queries, tensor maps
+            torch.cuda.current_stream(A.device).wait_stream(side)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                call(torch.cuda.current_stream(A.device))
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()
