@@ -5,6 +5,8 @@
 
 #include <atomic>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler is attached
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
 #error "this library is built for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
 #endif
@@ -17,6 +19,14 @@ inline std::atomic<uint64_t>& launch_counter() {
   return c;
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+
+// NVTX range for the life of a scope (ABI calls, Strassen levels): visible in nsys / ncu --nvtx
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Opt kernel KERN into `bytes` of dynamic shared memory on the CURRENT device, once per
 // (kernel, device): the attribute is per device, so a process driving several GPUs needs it on each.

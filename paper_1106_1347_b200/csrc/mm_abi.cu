@@ -101,6 +101,7 @@ const char* mm_status_string(int status) {
 int32_t mm_lambda(double nA, double nB) { return mmk::lambda_rule(nA, nB); }
 
 int mm_naive(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  mmk::NvtxRange nvtx("mm_naive");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   int sms = 148;
@@ -123,6 +124,7 @@ int mm_naive_ex(const double* A, int64_t lda, const double* B, int64_t ldb, doub
 }
 
 int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  mmk::NvtxRange nvtx("mm_kahan");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   int sms = 148;
@@ -131,6 +133,7 @@ int mm_kahan(const double* A, const double* B, double* C, int64_t N, int64_t P, 
 }
 
 int mm_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M, void* stream) {
+  mmk::NvtxRange nvtx("mm_kahan_fused");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   int sms = 148;
@@ -160,6 +163,7 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
 
 static int winograd_common(bool fused, const double* A, const double* B, double* C, int64_t N, int64_t P,
                            int64_t M, void* workspace, size_t ws_bytes, void* stream) {
+  mmk::NvtxRange nvtx(fused ? "mm_winograd_fused" : "mm_winograd");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
@@ -192,6 +196,7 @@ int mm_winograd_scaled(const double* A, const double* B, double* C, int64_t N, i
 static int winograd_scaled_common(bool fused, const double* A, const double* B, double* C, int64_t N, int64_t P,
                                   int64_t M, const double* norms_device, void* workspace, size_t ws_bytes,
                                   int32_t* lambda_out, void* stream) {
+  mmk::NvtxRange nvtx(fused ? "mm_winograd_scaled_fused" : "mm_winograd_scaled");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   if (!workspace) return MM_ERR_ARG;
@@ -244,6 +249,7 @@ int mm_strassen_plan(int64_t N, int64_t P, int64_t M, int32_t levels, int32_t* d
 
 static int strassen_common(int variant, const double* A, const double* B, double* C, int64_t N, int64_t P,
                            int64_t M, int32_t levels, void* workspace, size_t ws_bytes, void* stream) {
+  mmk::NvtxRange nvtx(variant == mmk::SV_NAIV ? "mm_strassen" : "mm_strassen_winograd");
   int rc = check_abc(A, B, C, N, P, M);
   if (rc) return rc;
   mmk::StrassenPlan pl;
@@ -345,6 +351,7 @@ size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M,
 int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, int64_t N_local, int64_t P,
                  int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
                  void* stream) {
+  mmk::NvtxRange nvtx("mm_dist_gemm");
   mmk::DistState& ds = mmk::dist_state();
   if (!ds.comm || !B || P < 1 || M < 1 || N_local < 0 || root < 0 || root >= ds.world) return MM_ERR_ARG;
   if (N_local > 0 && (!A_shard || !C_shard)) return MM_ERR_ARG;

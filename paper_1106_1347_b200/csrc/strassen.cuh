@@ -354,6 +354,7 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   double* Cb[2] = {reinterpret_cast<double*>(ws + pl.offC[0]), reinterpret_cast<double*>(ws + pl.offC[1])};
   // level l >= 1 of S/T lives in buffer (d - l) % 2 ; combination level l >= 1 in Cb[(d - 1 - l) % 2]
   for (int side = 0; side < 2; ++side) {
+    NvtxRange nvtx(side == 0 ? "strassen form (A side)" : "strassen form (B side)");
     const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
     double** buf = side == 0 ? S : T;
     for (int l = 0; l < d; ++l) {
@@ -383,11 +384,13 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   }
   // the 7^d leaf products, one batched DMMA launch
   {
+    NvtxRange nvtx("strassen leaf products");
     const int64_t n = pl.Np >> d, p = pl.Pp >> d, m = pl.Mp >> d;
     GemmProblem pr{S[0], T[0], Hb, n, p, m, p, m, m, n * p, p * m, n * m, ipow7(d)};
     e = launch_dgemm(pr, st, sms);
     if (e != cudaSuccess) return e;
   }
+  NvtxRange nvtx_combine("strassen combination");
   for (int l = d - 1; l >= 0; --l) {
     CombineArgs ca;
     const int64_t r_l = pl.Np >> l, c_l = pl.Mp >> l;
