@@ -130,13 +130,22 @@ def _operands(A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor]):
 _ws = {}
 
 
-def _workspace(nbytes: int, device) -> Tuple[int, int]:
+def _workspace(nbytes: int, device, stream=None) -> Tuple[int, int]:
+    """A scratch buffer of >= nbytes for calls enqueued on `stream` (default: the current stream).
+    One buffer per (device, stream): calls on different streams may run concurrently and must not
+    share scratch space; the buffer is allocated on that stream, so when it is replaced by a
+    larger one the caching allocator only recycles its memory in that stream's order."""
     if nbytes == 0:
         return 0, 0
-    key = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, s.cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        with torch.cuda.stream(s):
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         _ws[key] = buf
     return buf.data_ptr(), buf.numel()
 
@@ -170,7 +179,7 @@ def _gemm(method: int, name: str, A, B, out=None, levels: int = 0, stream=None, 
         d = strassen_plan(N, P, M, levels)[0]
         if d != 0:
             raise MMError("bad Strassen plan")
-    ws_ptr, ws_len = _workspace(ws_bytes, A.device)
+    ws_ptr, ws_len = _workspace(ws_bytes, A.device, stream)
     lam = ctypes.c_int32(0)
     st = _stream_handle(stream, A.device)
     with torch.cuda.device(A.device):  # the library launches on the current device
@@ -238,7 +247,7 @@ def winograd_scaled(A, B, *, out=None, stream=None, return_lambda: bool = False,
     if norms.dtype != torch.float64 or norms.numel() != 2 or norms.device != A.device or not norms.is_contiguous():
         raise ValueError("norms must be a contiguous 2-element float64 tensor on A's device")
     L = lib()
-    ws_ptr, ws_len = _workspace(int(L.mm_workspace_size(MM_WINOGRAD_SCALED, N, P, M, 0)), A.device)
+    ws_ptr, ws_len = _workspace(int(L.mm_workspace_size(MM_WINOGRAD_SCALED, N, P, M, 0)), A.device, stream)
     lam = ctypes.c_int32(0)
     with torch.cuda.device(A.device):
         rc = L.mm_winograd_scaled_norms(A.data_ptr(), B.data_ptr(), out.data_ptr(), N, P, M, norms.data_ptr(), ws_ptr,

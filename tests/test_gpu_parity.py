@@ -408,3 +408,30 @@ def test_c2_paper_plan_bitwise(method, c2_ops):
     assert np.array_equal(C, ref)
     lit = oracle_rows("naive_standard", A, B)
     assert norm_rows_err(C, lit) <= tol_for(method) * oracle.norm_inf(A) * oracle.norm_inf(B)
+
+
+def test_concurrent_streams_private_workspaces():
+    """Products enqueued on two streams at once (every method with a workspace) each get their own
+    scratch space: both results are bitwise their oracles."""
+    A1, B1 = workload.custom(700, 512, 600, seed=31)
+    A2, B2 = workload.custom(700, 512, 600, seed=32)
+    d = [(dev(A1), dev(B1)), (dev(A2), dev(B2))]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for name, ref in (("winograd", oracle.winograd_original), ("winograd_scaled", lambda a, b: oracle.winograd_scaled(a, b)[0]),
+                      ("strassen_winograd", None)):
+        outs = []
+        for r in range(3):  # interleave launches on the two streams
+            for (dA, dB), s in zip(d, streams):
+                with torch.cuda.stream(s):
+                    kw = {"levels": 2} if name.startswith("strassen") else {}
+                    outs.append(getattr(mm, name)(dA, dB, stream=s, **kw))
+        torch.cuda.synchronize()
+        for k, C in enumerate(outs):
+            A, B = (A1, B1) if k % 2 == 0 else (A2, B2)
+            if ref is None:
+                dpl, pad = plan_pad(700, 512, 600, 2)
+                expect = oracle.strassen(1, A, B, levels=dpl, pad=pad, base=oracle.BASE_FMA)
+            else:
+                expect = ref(A, B)
+            assert np.array_equal(C.cpu().numpy(), expect), (name, k)
