@@ -120,10 +120,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
-  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_s4_3cta_bk16", A, B, R, nullptr, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 2, 3, 32>, true>("tma_64x64_s2_3cta_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 3, 3, 32>, true>("tma_64x64_s3_3cta_bk32", A, B, C, R, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 2, 3, 32>, true>("tma_64x64_s2_3cta_bk32", A, B, R, nullptr, n, reps, bad);
+  run<GemmCfg<64, 64, 2, 2, 2, 2, 32>, true>("tma_64x64_s2_2cta_bk32", A, B, C, R, n, reps, bad);
   run<GemmCfg<64, 64, 2, 2, 3, 2, 32>, true>("tma_64x64_s3_2cta_bk32", A, B, C, R, n, reps, bad);
-  run<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_s4_3cta_bk16_again", A, B, C, R, n, reps, bad);
+  run<GemmCfg<128, 64, 4, 2, 2, 2, 32>, true>("tma_128x64_w4x2_s2_2cta_bk32", A, B, C, R, n, reps, bad);
   return 0;
 }
