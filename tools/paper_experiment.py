@@ -42,6 +42,10 @@ ROWS = [
 EXTRA = [
     ("StrassenNaiv (GPU plan, 2 levels)", "strassen", {"levels": 2}),
     ("StrassenWinograd (GPU plan, 2 levels)", "strassen_winograd", {"levels": 2}),
+    # the fused-FMA variants (not the paper's methods; reading R22)
+    ("NaivKahan (fused FMA)", "kahan_fused", {}),
+    ("WinogradOriginal (fused FMA)", "winograd_fused", {}),
+    ("WinogradScaled (fused FMA)", "winograd_scaled_fused", {}),
 ]
 
 
