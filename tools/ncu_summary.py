@@ -6,6 +6,7 @@ import csv
 import io
 import json
 import os
+import shutil
 import subprocess
 import sys
 
@@ -142,6 +143,10 @@ def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "pr
         f.write("\n".join(md) + "\n")
     with open(os.path.join(ROOT, "profiles", "kernel_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
+    # the raw ncu launch list and HBM-kernel metrics (small CSVs) travel with the summary
+    for name in ("launches.csv", "hbm_kernels.csv"):
+        if os.path.exists(os.path.join(src, name)):
+            shutil.copyfile(os.path.join(src, name), os.path.join(dst, "ncu_" + name))
     print("\n".join(md))
 
 
