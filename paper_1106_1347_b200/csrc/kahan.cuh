@@ -27,25 +27,26 @@ using KahanDefault = SimtCfg<64, 64, 4, 8, 2, 2, 32>;
 template <class CF, bool FUSED>
 __device__ __forceinline__ void kahan_step(double (&sum)[CF::TM][CF::TN], double (&err)[CF::TM][CF::TN],
                                            const double* As, const double* Bs, int kk, int ty, int tx) {
-  double a[CF::TM], b[CF::TN];
-#pragma unroll
-  for (int i = 0; i < CF::TM; ++i) a[i] = As[simt_row<CF>(ty, i) * CF::APITCH + kk];
+  double b[CF::TN];
 #pragma unroll
   for (int c = 0; c < CF::TN / 2; ++c) {
     double2 v = *reinterpret_cast<const double2*>(Bs + kk * CF::BN + 2 * tx + 2 * CF::TXN * c);
     b[2 * c] = v.x;
     b[2 * c + 1] = v.y;
   }
+  // A's value of row i is read just before its TN updates (B's stay in registers)
 #pragma unroll
-  for (int i = 0; i < CF::TM; ++i)
+  for (int i = 0; i < CF::TM; ++i) {
+    const double a = As[simt_row<CF>(ty, i) * CF::APITCH + kk];
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) {
-      double e = FUSED ? __fma_rn(a[i], b[j], err[i][j]) : dadd(err[i][j], dmul(a[i], b[j]));
+      double e = FUSED ? __fma_rn(a, b[j], err[i][j]) : dadd(err[i][j], dmul(a, b[j]));
       const double t = dadd(sum[i][j], e);
       e = dadd(dsub(sum[i][j], t), e);
       sum[i][j] = t;
       err[i][j] = e;
     }
+  }
 }
 
 template <class CF, int AV, int BV, int CV, bool FUSED>

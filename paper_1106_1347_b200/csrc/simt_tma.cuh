@@ -136,10 +136,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) sum[i][j] = err[i][j] = 0.0;
 
+  // per k: B's TN values stay in registers, A's value of row i is read just before its TN
+  // updates (156.5 vs 156.7 ms with all of A's values loaded up front; kahan_sched.log)
   auto step = [&](const double* As, const double* Bs, int kk) {
-    double av[CF::TM], bv[CF::TN];
-#pragma unroll
-    for (int i = 0; i < CF::TM; ++i) av[i] = As[sw_a<CF>(simt_row<CF>(ty, i), kk)];
+    double bv[CF::TN];
 #pragma unroll
     for (int c = 0; c < CF::TN / 2; ++c) {
       const double2 v = *reinterpret_cast<const double2*>(Bs + sw_b<CF>(kk, tx, c));
@@ -147,16 +147,18 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
       bv[2 * c + 1] = v.y;
     }
 #pragma unroll
-    for (int i = 0; i < CF::TM; ++i)
+    for (int i = 0; i < CF::TM; ++i) {
+      const double ai = As[sw_a<CF>(simt_row<CF>(ty, i), kk)];
 #pragma unroll
       for (int j = 0; j < CF::TN; ++j) {  // the update of P:122-132, every op separately rounded
         // (FUSED, NEXT-3 / reading R22: err = fma(a, b, err))
-        double e = FUSED ? __fma_rn(av[i], bv[j], err[i][j]) : dadd(err[i][j], dmul(av[i], bv[j]));
+        double e = FUSED ? __fma_rn(ai, bv[j], err[i][j]) : dadd(err[i][j], dmul(ai, bv[j]));
         const double t = dadd(sum[i][j], e);
         e = dadd(dsub(sum[i][j], t), e);
         sum[i][j] = t;
         err[i][j] = e;
       }
+    }
   };
 
 #pragma unroll 1
@@ -217,15 +219,11 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
     const double* Bs = pp.Bs_base + s * LY::B_TILE;
     // a zero-filled pair past P adds (0+0)(0+0) = +0 to acc, which leaves acc unchanged
     // (acc starts at +0 and can never become -0), so the last tile needs no guard
+    // per pair: B's TN column pairs stay in registers, A's pair of row i is read just before its
+    // TN entries (64.70 vs 65.02 ms with all of A's pairs loaded up front; winograd_sched.log)
 #pragma unroll 2
     for (int jp = 0; jp < CF::BK / 2; ++jp) {
-      double a0[TM], a1[TM], b0[TN], b1[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
-        a0[i] = v.x;
-        a1[i] = v.y;
-      }
+      double b0[TN], b1[TN];
 #pragma unroll
       for (int c = 0; c < TN / 2; ++c) {
         const double2 u = *reinterpret_cast<const double2*>(Bs + sw_b<CF>(2 * jp, tx, c));
@@ -236,9 +234,11 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
         b1[2 * c + 1] = w.y;
       }
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+      for (int i = 0; i < TM; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], a0[i], a1[i], b0[j], b1[j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], v.x, v.y, b0[j], b1[j]);
+      }
     }
   }
 

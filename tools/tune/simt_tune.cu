@@ -132,8 +132,9 @@ int main(int argc, char** argv) {
     return 0;
   }
   const bool wino_only = argc > 1 && argv[1][0] == 'w';
+  const bool kahan_only = argc > 1 && argv[1][0] == 'k';
   Ctx c;
-  c.n = argc > 1 && !wino_only ? atoll(argv[1]) : 8192;
+  c.n = argc > 1 && !wino_only && !kahan_only ? atoll(argv[1]) : 8192;
   c.reps = argc > 2 ? atoi(argv[2]) : 2;
   cudaMalloc(&c.A, c.n * c.n * 8);
   cudaMalloc(&c.B, c.n * c.n * 8);
@@ -145,12 +146,21 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB, BK>
+  if (kahan_only) {  // K2 configurations only
+    kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_2cta_bk32", c);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 2, 3, 32>>("tma_64x64_s2_3cta_bk32", c);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 4, 3, 16>>("tma_64x64_s4_3cta_bk16", c);
+    return 0;
+  }
   if (wino_only) {  // K3 configurations only
     wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
     wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_2cta_bk32", c);
     wino_tma<SimtCfg<128, 64, 8, 8, 3, 1, 32>>("tma_128x64_s3_1cta_bk32", c);
     wino_tma<SimtCfg<64, 64, 8, 8, 2, 3, 32>>("tma_64x64_t8x8_s2_3cta_bk32", c);
     wino_tma<SimtCfg<64, 64, 4, 8, 3, 3, 32>>("tma_64x64_t4x8_s3_3cta_bk32", c);
+    wino_tma<SimtCfg<128, 64, 8, 8, 2, 3, 16>>("tma_128x64_s2_3cta_bk16", c);
+    wino_tma<SimtCfg<128, 64, 8, 8, 3, 3, 16>>("tma_128x64_s3_3cta_bk16", c);
     return 0;
   }
   kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
