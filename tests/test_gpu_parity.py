@@ -435,3 +435,20 @@ def test_concurrent_streams_private_workspaces():
             else:
                 expect = ref(A, B)
             assert np.array_equal(C.cpu().numpy(), expect), (name, k)
+
+
+# ------------------------------------------------------------------ deepest recursion the ABI accepts
+@pytest.mark.parametrize("levels", [4, 5, 6, 7, 8])
+def test_strassen_deep_levels_bitwise(levels):
+    """levels up to the ABI's maximum (8): every dimension padded to a multiple of 2^(d+1), 7^d
+    leaves of 2x2x2 at d = 8 (5.8 million batched leaf problems), bitwise the oracle's plan."""
+    N, P, M = 5, 3, 7
+    A, B = workload.custom(N, P, M, seed=500 + levels)
+    dA, dB = dev(A), dev(B)
+    for name, v in (("strassen", 0), ("strassen_winograd", 1)):
+        d, pad = plan_pad(N, P, M, levels)
+        assert d == levels
+        C = host(run(name, dA, dB, levels))
+        ref = oracle.strassen(v, A, B, levels=d, pad=pad, base=oracle.BASE_FMA)
+        assert np.array_equal(C, ref), (name, levels)
+    mm.release_workspace()
