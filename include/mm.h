@@ -89,6 +89,34 @@ int mm_naive_ex(const double* A, int64_t lda, const double* B, int64_t ldb, doub
                 int64_t K, int64_t M, int32_t accumulate, void* stream);
 
 /*
+ * k-panel steps of NaivKahan and WinogradOriginal (B broadcast in row panels
+ * overlapped with the products; mm_dist_gemm uses them).  A is N x K with row pitch lda >= K, B is
+ * K x M with pitch ldb >= M (panel views of wider operands), C (and E) dense N x M.  Flags:
+ *   MM_EX_ACCUMULATE  each entry's running state starts from the previous panel's (C, and E for
+ *                     Kahan) instead of +0, and continues over k = 0..K-1 in order;
+ *   MM_EX_KEEP_STATE  the running state is stored for a later panel: Kahan writes `sum` into C and
+ *                     `err` into E; Winograd writes the raw pair sum into C (no epilogue);
+ *   MM_EX_FUSED       the NEXT-3 variant (reading R22).
+ * Running the panels of P in increasing k -- the first without ACCUMULATE, all but the last with
+ * KEEP_STATE -- performs every entry's operations in exactly the one-shot order, so the result is
+ * bit for bit mm_kahan / mm_winograd (or the fused variants).  Requirements (else MM_ERR_ARG):
+ * A and B 16-byte aligned, lda, ldb and M even (the TMA-fed kernels), and for Winograd K even
+ * (whole pairs per panel) and y, z (mm_winograd_yz of the FULL operands) unless KEEP_STATE.
+ * No workspace; E is caller-owned (N x M doubles) and required with ACCUMULATE or KEEP_STATE.
+ */
+#define MM_EX_ACCUMULATE 1
+#define MM_EX_KEEP_STATE 2
+#define MM_EX_FUSED 4
+int mm_kahan_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, double* E, int64_t N,
+                int64_t K, int64_t M, int32_t flags, void* stream);
+int mm_winograd_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, const double* y,
+                   const double* z, int64_t N, int64_t K, int64_t M, int32_t flags, void* stream);
+/* y_i and z_k of P:189 (sums in increasing j; fma when flags & MM_EX_FUSED) of dense A (N x P) and
+ * B (P x M) into device vectors y (N) and z (M). */
+int mm_winograd_yz(const double* A, const double* B, int64_t N, int64_t P, int64_t M, double* y, double* z,
+                   int32_t flags, void* stream);
+
+/*
  * mm_kahan -- NaivKahan: each entry is the compensated sum of the products
  * A_ik B_kj, k increasing, with the update of P:122-132
  * (err = err + x; t = sum + err; err = (sum - t) + err; sum = t), result `sum`.
@@ -205,9 +233,13 @@ int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_
  * mm_dist_gemm -- C_shard = A_shard B for this rank's N_local rows (N_local >= 0; a rank without
  *   rows still takes part in the collectives).  B: DEVICE buffer P x M on every rank; the root's
  *   content is broadcast into it in place inside the call.  method: an mm_method id.  For
- *   MM_NAIVE with panels > 1, B travels as `panels` (<= 64) row panels on the layer's own stream
- *   and the product accumulates panel by panel (mm_naive_ex), each panel's multiply waiting only
- *   for its own transfer -- bitwise the one-shot product.  WinogradScaled uses the global
+ *   MM_NAIVE, MM_KAHAN[_FUSED] and MM_WINOGRAD[_FUSED] with panels > 1, B travels as `panels`
+ *   (<= 64, even boundaries) row panels on the layer's own stream and the product accumulates
+ *   panel by panel (mm_naive_ex / mm_kahan_ex with the carried err in the workspace /
+ *   mm_winograd_ex, y and z of the full operands computed once the last panel has landed), each
+ *   panel's step waiting only for its own transfer -- bitwise the one-shot product.  Kahan and
+ *   Winograd take the panel path only for 16-byte aligned operands with P and M even (else one
+ *   broadcast, then the one-shot kernel).  WinogradScaled uses the global
  *   ||A||_inf (max-all-reduce of the row blocks' norms) and the local ||B||_inf, so lambda equals
  *   the one-GPU lambda.  Classical, Kahan and both Winograds are bitwise the rows of the one-GPU
  *   product; Strassen recurses on the shard (within its tolerance).  workspace: DEVICE, >=

@@ -70,7 +70,11 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).restype = ctypes.c_int
         L.or_naive_unroll.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64]
         L.or_naive_fma_acc.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, i64]
+        L.or_naive_kahan_acc.argtypes = [dp, i64, dp, i64, dp, dp, i64, i64, i64, ctypes.c_int]
+        L.or_winograd_pairs_acc.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, ctypes.c_int]
+        L.or_winograd_finish.argtypes = [dp, dp, dp, dp, i64, i64]
         L.or_winograd_yz.argtypes = [dp, dp, dp, dp, i64, i64, i64]
+        L.or_winograd_yz_fused.argtypes = [dp, dp, dp, dp, i64, i64, i64]
         L.or_lambda.argtypes = [d, d]
         L.or_lambda.restype = ctypes.c_int
         L.or_winograd_scaled.argtypes = [dp, dp, dp, i64, i64, i64, ctypes.POINTER(i32)]
@@ -189,6 +193,62 @@ def naive_fma_acc(A, B, C):
     if rc != 0:
         raise ValueError("or_naive_fma_acc failed")
     return C
+
+
+def _panel_args(A, B, *dense):
+    for X in (A, B):
+        if X.dtype != np.float64 or X.ndim != 2 or X.strides[1] != 8:
+            raise ValueError("row-major float64 matrices with unit column stride required")
+    N, K = A.shape
+    M = B.shape[1]
+    for X in dense:
+        if X.dtype != np.float64 or X.shape != (N, M) or not X.flags.c_contiguous:
+            raise ValueError("state arrays must be dense float64 N x M")
+    if B.shape[0] != K:
+        raise ValueError("shape mismatch")
+    return N, K, M
+
+
+def naive_kahan_acc(A, B, S, E, fused: bool = False):
+    """NaivKahan's update resumed from the state (S = sum, E = err; modified in
+    place) over a k-panel A (N x K view), B (K x M view): the NEXT-4 panel step."""
+    N, K, M = _panel_args(A, B, S, E)
+    if lib().or_naive_kahan_acc(_dp(A), A.strides[0] // 8, _dp(B), B.strides[0] // 8, _dp(S), _dp(E), N, K, M,
+                                int(fused)) != 0:
+        raise ValueError("or_naive_kahan_acc failed")
+    return S, E
+
+
+def winograd_pairs_acc(A, B, Acc, fused: bool = False):
+    """WinogradOriginal's pair sum resumed from Acc (modified in place) over the
+    K/2 pairs of a k-panel (K even)."""
+    N, K, M = _panel_args(A, B, Acc)
+    if lib().or_winograd_pairs_acc(_dp(A), A.strides[0] // 8, _dp(B), B.strides[0] // 8, _dp(Acc), N, K, M,
+                                   int(fused)) != 0:
+        raise ValueError("or_winograd_pairs_acc failed")
+    return Acc
+
+
+def winograd_finish(Acc, y, z):
+    """The even-P epilogue C = (acc - y_i) - z_k."""
+    N, M = Acc.shape
+    C = np.empty((N, M), dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    if y.shape != (N,) or z.shape != (M,):
+        raise ValueError("y, z must have N and M entries")
+    if lib().or_winograd_finish(_dp(np.ascontiguousarray(Acc)), _dp(y), _dp(z), _dp(C), N, M) != 0:
+        raise ValueError("or_winograd_finish failed")
+    return C
+
+
+def winograd_yz_fused(A, B):
+    """y, z of P:189 accumulated by fma (NEXT-3, reading R22)."""
+    A, B, N, P, M = _ab(A, B)
+    y = np.empty((N,), dtype=np.float64)
+    z = np.empty((M,), dtype=np.float64)
+    lib().or_winograd_yz_fused(_dp(A), _dp(B), _dp(y), _dp(z), N, P, M)
+    return y, z
 
 
 def naive_kahan_fused(A, B):

@@ -187,6 +187,33 @@ int or_naive_fma_acc(const double* A, int64_t lda, const double* B, int64_t ldb,
   return 0;
 }
 
+/* NEXT-4 for NaivKahan: the loop of P:122-132 (fused: err = fma(a, b, err), reading R22) resumed
+ * from a given state -- sum = S_ij, err = E_ij -- over k = 0..K-1 of strided panels; the state is
+ * written back.  Consecutive k-panels started from (0, 0) therefore compose to or_naive_kahan. */
+int or_naive_kahan_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* S, double* E,
+                       int64_t N, int64_t K, int64_t M, int fused) {
+  int64_t i, j, k;
+  if (!A || !B || !S || !E || N < 1 || K < 1 || M < 1 || lda < K || ldb < M) return -1;
+  for (i = 0; i < N; i++)
+    for (j = 0; j < M; j++) {
+      double t, sum = S[i * M + j], err = E[i * M + j];
+      for (k = 0; k < K; k++) {
+        if (fused) {
+          err = fma(A[i * lda + k], B[k * ldb + j], err);
+        } else {
+          double x = A[i * lda + k] * B[k * ldb + j];
+          err = err + x;
+        }
+        t = sum + err;
+        err = (sum - t) + err;
+        sum = t;
+      }
+      S[i * M + j] = sum;
+      E[i * M + j] = err;
+    }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ Section 2.3 */
 static double winograd_y(const double* A, int64_t P, int64_t i) {
   double y = 0.0;
@@ -234,6 +261,34 @@ int or_winograd_original(const double* A, const double* B, double* C, int64_t N,
     for (k = 0; k < M; k++) C[IDX(i, k, M)] = winograd_entry_yz(A, B, P, M, i, k, y[i], z[k]);
   free(y);
   free(z);
+  return 0;
+}
+
+/* NEXT-4 for WinogradOriginal: the pair sum of P:189-192 (fused: acc = fma(.., .., acc)) resumed
+ * from Acc_ik over the K/2 pairs of a strided k-panel (K even), written back; and the epilogue
+ * C = (acc - y_i) - z_k of an even-P product. */
+int or_winograd_pairs_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* Acc, int64_t N,
+                          int64_t K, int64_t M, int fused) {
+  int64_t i, k, j;
+  if (!A || !B || !Acc || N < 1 || K < 2 || K % 2 || M < 1 || lda < K || ldb < M) return -1;
+  for (i = 0; i < N; i++)
+    for (k = 0; k < M; k++) {
+      double acc = Acc[i * M + k];
+      for (j = 0; j < K / 2; j++) {
+        double u = A[i * lda + 2 * j] + B[(2 * j + 1) * ldb + k];
+        double v = A[i * lda + 2 * j + 1] + B[(2 * j) * ldb + k];
+        acc = fused ? fma(u, v, acc) : acc + u * v;
+      }
+      Acc[i * M + k] = acc;
+    }
+  return 0;
+}
+
+int or_winograd_finish(const double* Acc, const double* y, const double* z, double* C, int64_t N, int64_t M) {
+  int64_t i, k;
+  if (!Acc || !y || !z || !C || N < 1 || M < 1) return -1;
+  for (i = 0; i < N; i++)
+    for (k = 0; k < M; k++) C[i * M + k] = (Acc[i * M + k] - y[i]) - z[k];
   return 0;
 }
 
@@ -529,6 +584,14 @@ static double winograd_entry_yz_fused(const double* A, const double* B, int64_t 
   c = (acc - yi) - zk;
   if (P % 2 == 1) c = fma(A[IDX(i, P - 1, P)], B[IDX(P - 1, k, M)], c);
   return c;
+}
+
+int or_winograd_yz_fused(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M) {
+  int64_t i, k;
+  if (bad_dims(A, B, y, N, P, M) || z == NULL) return -1;
+  for (i = 0; i < N; i++) y[i] = winograd_y_fused(A, P, i);
+  for (k = 0; k < M; k++) z[k] = winograd_z_fused(B, P, M, k);
+  return 0;
 }
 
 int or_naive_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M) {

@@ -68,6 +68,11 @@ int or_naive_fma(const double* A, const double* B, double* C, int64_t N, int64_t
 int or_naive_fma_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                      int64_t N, int64_t K, int64_t M);
 
+/* NEXT-4: NaivKahan's update (fused != 0: err = fma(a, b, err)) resumed from the state
+ * (S = sum, E = err, both N x M dense) over a strided k-panel; writes the state back. */
+int or_naive_kahan_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* S, double* E,
+                       int64_t N, int64_t K, int64_t M, int fused);
+
 /* ---- Section 2.3: Winograd ---- */
 /* gamma = floor(P/2); y_i = sum_{j<gamma} A[i][2j]*A[i][2j+1];
  * z_k = sum_{j<gamma} B[2j][k]*B[2j+1][k]  (0-based form of A_{i,2j-1}A_{i,2j}) */
@@ -75,6 +80,12 @@ int or_winograd_yz(const double* A, const double* B, double* y, double* z, int64
 /* P:187-195 (WinogradOriginal): C_ik = (acc - y_i) - z_k  [+ A[i][P-1]*B[P-1][k] if P odd],
  * acc = sum_{j<gamma} (A[i][2j] + B[2j+1][k]) * (A[i][2j+1] + B[2j][k]) */
 int or_winograd_original(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
+/* NEXT-4: WinogradOriginal's pair sum resumed from Acc (N x M) over the K/2 pairs of a
+ * strided k-panel (K even); fused != 0: acc = fma(u, v, acc).  or_winograd_finish: the even-P
+ * epilogue C = (acc - y_i) - z_k. */
+int or_winograd_pairs_acc(const double* A, int64_t lda, const double* B, int64_t ldb, double* Acc, int64_t N,
+                          int64_t K, int64_t M, int fused);
+int or_winograd_finish(const double* Acc, const double* y, const double* z, double* C, int64_t N, int64_t M);
 /* the integer lambda with 1/2 <= 2^lambda nA / (2^-lambda nB) <= 2,
  * exact (frexp); ties (both lambdas valid) -> the larger |lambda|; nA or nB == 0 -> 0. */
 int or_lambda(double nA, double nB);
@@ -88,6 +99,8 @@ int or_winograd_scaled(const double* A, const double* B, double* C, int64_t N, i
  * fma(x, y, s); all other operations and all orders are the method's own. ---- */
 /* NaivKahan with err = fma(A_ik, B_kj, err) */
 int or_naive_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
+/* y, z of P:189 accumulated by fma (the y/z of or_winograd_fused) */
+int or_winograd_yz_fused(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M);
 /* WinogradOriginal with y, z, acc and the odd-P term accumulated by fma */
 int or_winograd_fused(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M);
 /* WinogradScaled on top of or_winograd_fused */

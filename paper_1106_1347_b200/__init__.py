@@ -44,7 +44,9 @@ EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winogra
            "mm_strassen", "mm_strassen_winograd", "mm_strassen_plan", "mm_workspace_size", "mm_gemm", "norm_inf",
            "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
            "mm_winograd_scaled_fused", "mm_naive_ex", "mm_dist_get_unique_id", "mm_dist_init",
-           "mm_dist_workspace_size", "mm_dist_gemm", "mm_dist_finalize")
+           "mm_dist_workspace_size", "mm_dist_gemm", "mm_dist_finalize", "mm_kahan_ex", "mm_winograd_ex",
+           "mm_winograd_yz")
+MM_EX_ACCUMULATE, MM_EX_KEEP_STATE, MM_EX_FUSED = 1, 2, 4
 
 
 class MMError(RuntimeError):
@@ -69,6 +71,9 @@ def lib() -> ctypes.CDLL:
         for n in ("mm_naive", "mm_kahan", "mm_kahan_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp]
         L.mm_naive_ex.argtypes = [dp, i64, dp, i64, dp, i64, i64, i64, i64, i32, vp]
+        L.mm_kahan_ex.argtypes = [dp, i64, dp, i64, dp, dp, i64, i64, i64, i32, vp]
+        L.mm_winograd_ex.argtypes = [dp, i64, dp, i64, dp, dp, dp, i64, i64, i64, i32, vp]
+        L.mm_winograd_yz.argtypes = [dp, dp, i64, i64, i64, dp, dp, i32, vp]
         L.mm_dist_get_unique_id.argtypes = [ctypes.c_char_p]
         L.mm_dist_init.argtypes = [i32, i32, ctypes.c_char_p, i32]
         L.mm_dist_workspace_size.argtypes = [ctypes.c_int, i64, i64, i64, i32]
@@ -214,6 +219,66 @@ def naive_panel(A, B, C, *, accumulate: bool, stream=None):
         rc = lib().mm_naive_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), N,
                                K, M, 1 if accumulate else 0, _stream_handle(stream, A.device))
     _check(rc, "mm_naive_ex")
+    return C
+
+
+def _panel_views(A, B, C, E=None):
+    for t in (A, B, C) + ((E,) if E is not None else ()):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.dim() == 2
+                and t.stride(1) == 1):
+            raise ValueError("operands must be row-major float64 CUDA matrices (unit column stride)")
+    N, K = A.shape
+    M = B.shape[1]
+    if B.shape[0] != K or C.shape != (N, M) or not C.is_contiguous():
+        raise ValueError(f"shape mismatch or non-dense C: {tuple(A.shape)} x {tuple(B.shape)} -> {tuple(C.shape)}")
+    if E is not None and (E.shape != (N, M) or not E.is_contiguous()):
+        raise ValueError("E must be a dense N x M float64 tensor")
+    if not (A.device == B.device == C.device):
+        raise ValueError("operands must be on one device")
+    return N, K, M
+
+
+def _ex_flags(accumulate, keep_state, fused):
+    return (MM_EX_ACCUMULATE if accumulate else 0) | (MM_EX_KEEP_STATE if keep_state else 0) | (
+        MM_EX_FUSED if fused else 0)
+
+
+def kahan_panel(A, B, C, E, *, accumulate: bool, keep_state: bool, fused: bool = False, stream=None):
+    """One k-panel of NaivKahan (mm_kahan_ex): A / B are panel views (A[:, k0:k1], B[k0:k1]), C and E
+    dense N x M holding each entry's (sum, err); consecutive panels, the first without
+    `accumulate` and all but the last with `keep_state`, reproduce kahan() bit for bit."""
+    N, K, M = _panel_views(A, B, C, E)
+    with torch.cuda.device(A.device):
+        rc = lib().mm_kahan_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(),
+                               E.data_ptr() if E is not None else None, N, K, M,
+                               _ex_flags(accumulate, keep_state, fused), _stream_handle(stream, A.device))
+    _check(rc, "mm_kahan_ex")
+    return C
+
+
+def winograd_yz(A, B, y, z, *, fused: bool = False, stream=None):
+    """y_i, z_k of WinogradOriginal for dense A, B into device vectors y (N), z (M)."""
+    N, P = A.shape
+    M = B.shape[1]
+    for t, n in ((y, N), (z, M)):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == n):
+            raise ValueError("y, z must be contiguous float64 CUDA vectors of N and M entries")
+    with torch.cuda.device(A.device):
+        rc = lib().mm_winograd_yz(A.data_ptr(), B.data_ptr(), N, P, M, y.data_ptr(), z.data_ptr(),
+                                  MM_EX_FUSED if fused else 0, _stream_handle(stream, A.device))
+    _check(rc, "mm_winograd_yz")
+
+
+def winograd_panel(A, B, C, y=None, z=None, *, accumulate: bool, keep_state: bool, fused: bool = False,
+                   stream=None):
+    """One k-panel (even width) of WinogradOriginal's pair sums (mm_winograd_ex); the last panel
+    (keep_state=False) applies C = (acc - y_i) - z_k with y, z of the full operands."""
+    N, K, M = _panel_views(A, B, C)
+    with torch.cuda.device(A.device):
+        rc = lib().mm_winograd_ex(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(),
+                                  y.data_ptr() if y is not None else None, z.data_ptr() if z is not None else None,
+                                  N, K, M, _ex_flags(accumulate, keep_state, fused), _stream_handle(stream, A.device))
+    _check(rc, "mm_winograd_ex")
     return C
 
 

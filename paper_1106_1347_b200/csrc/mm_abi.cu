@@ -141,6 +141,64 @@ int mm_kahan_fused(const double* A, const double* B, double* C, int64_t N, int64
   return cuda_status(mmk::launch_kahan<void, true>(A, B, C, N, P, M, S(stream), sms));
 }
 
+// k-panel steps of NaivKahan / WinogradOriginal: TMA-describable operands only
+static int ex_check(const double* A, int64_t lda, const double* B, int64_t ldb, const double* C, int64_t N,
+                    int64_t K, int64_t M, int32_t flags) {
+  if (!A || !B || !C || N < 1 || K < 1 || M < 1 || lda < K || ldb < M) return MM_ERR_ARG;
+  if (flags & ~(MM_EX_ACCUMULATE | MM_EX_KEEP_STATE | MM_EX_FUSED)) return MM_ERR_ARG;
+  if (!mul_ok(N, lda) || !mul_ok(K, ldb) || !mul_ok(N, M)) return MM_ERR_ARG;
+  if (!mmk::simt_tma_ex_ok(A, lda, B, ldb, N, K, M)) return MM_ERR_ARG;
+  const int64_t na = (N - 1) * lda + K, nb = (K - 1) * ldb + M;
+  if (overlaps(C, N * M, A, na) || overlaps(C, N * M, B, nb)) return MM_ERR_ALIAS;
+  return MM_OK;
+}
+
+static int ex_flags(int32_t flags) {
+  return ((flags & MM_EX_ACCUMULATE) ? mmk::SIMT_EX_ACC : 0) | ((flags & MM_EX_KEEP_STATE) ? mmk::SIMT_EX_KEEP : 0);
+}
+
+int mm_kahan_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, double* E, int64_t N,
+                int64_t K, int64_t M, int32_t flags, void* stream) {
+  mmk::NvtxRange nvtx("mm_kahan_ex");
+  int rc = ex_check(A, lda, B, ldb, C, N, K, M, flags);
+  if (rc) return rc;
+  if ((flags & (MM_EX_ACCUMULATE | MM_EX_KEEP_STATE)) && !E) return MM_ERR_ARG;
+  if (E && (overlaps(E, N * M, C, N * M) || overlaps(E, N * M, A, (N - 1) * lda + K) ||
+            overlaps(E, N * M, B, (K - 1) * ldb + M)))
+    return MM_ERR_ALIAS;
+  if ((rc = check_device(nullptr))) return rc;
+  const int f = ex_flags(flags);
+  return cuda_status((flags & MM_EX_FUSED)
+                         ? mmk::launch_kahan_tma_ex<mmk::KahanTma, true>(A, lda, B, ldb, C, E, N, K, M, f, S(stream))
+                         : mmk::launch_kahan_tma_ex<mmk::KahanTma, false>(A, lda, B, ldb, C, E, N, K, M, f, S(stream)));
+}
+
+int mm_winograd_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, const double* y,
+                   const double* z, int64_t N, int64_t K, int64_t M, int32_t flags, void* stream) {
+  mmk::NvtxRange nvtx("mm_winograd_ex");
+  int rc = ex_check(A, lda, B, ldb, C, N, K, M, flags);
+  if (rc) return rc;
+  if (K % 2 != 0) return MM_ERR_ARG;  // whole pairs per panel
+  if (!(flags & MM_EX_KEEP_STATE) && (!y || !z)) return MM_ERR_ARG;
+  if ((rc = check_device(nullptr))) return rc;
+  const int f = ex_flags(flags);
+  return cuda_status(
+      (flags & MM_EX_FUSED)
+          ? mmk::launch_winograd_tma_ex<mmk::WinogradTma, true>(A, lda, B, ldb, C, y, z, N, K, M, f, S(stream))
+          : mmk::launch_winograd_tma_ex<mmk::WinogradTma, false>(A, lda, B, ldb, C, y, z, N, K, M, f, S(stream)));
+}
+
+int mm_winograd_yz(const double* A, const double* B, int64_t N, int64_t P, int64_t M, double* y, double* z,
+                   int32_t flags, void* stream) {
+  mmk::NvtxRange nvtx("mm_winograd_yz");
+  if (!A || !B || !y || !z || N < 1 || P < 1 || M < 1 || !mul_ok(N, P) || !mul_ok(P, M)) return MM_ERR_ARG;
+  if (flags & ~MM_EX_FUSED) return MM_ERR_ARG;
+  int rc = check_device(nullptr);
+  if (rc) return rc;
+  return cuda_status(mmk::launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, S(stream),
+                                    (flags & MM_EX_FUSED) != 0));
+}
+
 size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels) {
   if (N < 1 || P < 1 || M < 1) return 0;
   switch (method) {
@@ -345,6 +403,8 @@ size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M,
   const int64_t n = N_local > 0 ? N_local : 1;
   if (method == MM_WINOGRAD_SCALED || method == MM_WINOGRAD_SCALED_FUSED)
     return kDistHeader + mm_workspace_size(method, n, P, M, levels);
+  if (method == MM_KAHAN || method == MM_KAHAN_FUSED)  // E, the carried err of the panel schedule
+    return mul_ok(n, M) ? mmk::align256(size_t(n) * size_t(M) * 8) : 0;
   return mm_workspace_size(method, n, P, M, levels);
 }
 
@@ -362,8 +422,18 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
   mmk::NcclApi* api = mmk::nccl_api();
   cudaStream_t st = S(stream);
   const size_t count = size_t(P) * size_t(M);
-  if (method == MM_NAIVE && panels > 1) {
-    // NEXT-4: panel i of B crosses NVLink on the comm stream while panel i-1 is multiplied
+  const bool kahan = method == MM_KAHAN || method == MM_KAHAN_FUSED;
+  const bool wino = method == MM_WINOGRAD || method == MM_WINOGRAD_FUSED;
+  const bool fused = method == MM_KAHAN_FUSED || method == MM_WINOGRAD_FUSED;
+  // the panel steps of Kahan / Winograd need the TMA-fed kernels (16-byte aligned, P and M even);
+  // other operands take the one-broadcast path below
+  const bool panel_ok = method == MM_NAIVE ||
+                        ((kahan || wino) && (N_local == 0 || mmk::simt_tma_ex_ok(A_shard, P, B, M, N_local, P, M)) &&
+                         P % 2 == 0 && M % 2 == 0);
+  if (panels > 1 && panel_ok) {
+    // NEXT-4: panel i of B crosses NVLink on the comm stream while panel i-1 is multiplied; every
+    // entry's running state (DMMA chain / Kahan (sum, err) / Winograd pair sum) continues from
+    // panel to panel in k order, so the shard is bitwise the one-shot product
     int64_t bounds[mmk::DistState::kMaxPanels + 1];
     const int np = mmk::dist_panel_bounds(P, panels, bounds);
     cudaError_t e = cudaEventRecord(ds.start_ev, st);  // B may be rewritten once prior work on st is done
@@ -376,11 +446,25 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
         return MM_ERR_NCCL;
       if ((e = cudaEventRecord(ds.panel_ev[i], ds.comm_stream)) != cudaSuccess) return cuda_status(e);
     }
+    double* E = static_cast<double*>(workspace);  // Kahan: the carried err
+    double* y = static_cast<double*>(workspace);  // Winograd: y, z of the full operands
+    double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N_local) * 8));
+    const int32_t fx = fused ? MM_EX_FUSED : 0;
     for (int i = 0; i < np; ++i) {
       if ((e = cudaStreamWaitEvent(st, ds.panel_ev[i], 0)) != cudaSuccess) return cuda_status(e);
       if (N_local == 0) continue;
-      const int rc = mm_naive_ex(A_shard + bounds[i], P, B + bounds[i] * M, M, C_shard, M, N_local,
-                                 bounds[i + 1] - bounds[i], M, i > 0 ? 1 : 0, stream);
+      const int64_t k0 = bounds[i], kw = bounds[i + 1] - bounds[i];
+      const bool last = i == np - 1;
+      const int32_t fl = fx | (i > 0 ? MM_EX_ACCUMULATE : 0) | (last ? 0 : MM_EX_KEEP_STATE);
+      int rc;
+      if (kahan) {
+        rc = mm_kahan_ex(A_shard + k0, P, B + k0 * M, M, C_shard, E, N_local, kw, M, fl, stream);
+      } else if (wino) {
+        if (last && (rc = mm_winograd_yz(A_shard, B, N_local, P, M, y, z, fx, stream))) return rc;
+        rc = mm_winograd_ex(A_shard + k0, P, B + k0 * M, M, C_shard, y, z, N_local, kw, M, fl, stream);
+      } else {
+        rc = mm_naive_ex(A_shard + k0, P, B + k0 * M, M, C_shard, M, N_local, kw, M, i > 0 ? 1 : 0, stream);
+      }
       if (rc) return rc;
     }
     return MM_OK;

@@ -32,7 +32,13 @@ struct SimtTmaArgs {
   const double* y;
   const double* z;
   int64_t N, P, M;
+  // k-panel continuation (mm_kahan_ex / mm_winograd_ex): SIMT_EX_ACC starts
+  // every entry's running state from C (and Kahan's err from E) instead of +0; SIMT_EX_KEEP
+  // stores the running state (Kahan: err into E; Winograd: the raw pair sum, no epilogue)
+  double* E;
+  int flags;
 };
+constexpr int SIMT_EX_ACC = 1, SIMT_EX_KEEP = 2;
 
 template <class CF>
 struct SimtTmaLayout {
@@ -135,6 +141,20 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
   for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) sum[i][j] = err[i][j] = 0.0;
+  if (a.flags & SIMT_EX_ACC) {  // continue each entry's (sum, err) from the previous k-panel
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) {
+      const int64_t row = m0 + simt_row<CF>(ty, i);
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j) {
+        const int64_t col = n0 + 2 * tx + 2 * CF::TXN * (j / 2) + (j & 1);
+        if (row < a.N && col < a.M) {
+          sum[i][j] = a.C[row * a.M + col];
+          err[i][j] = a.E[row * a.M + col];
+        }
+      }
+    }
+  }
 
   // per k: B's TN values stay in registers, A's value of row i is read just before its TN
   // updates (156.5 vs 156.7 ms with all of A's values loaded up front; kahan_sched.log)
@@ -189,12 +209,16 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
         if (col < a.M) a.C[row * a.M + col] = sum[i][2 * c];
         if (col + 1 < a.M) a.C[row * a.M + col + 1] = sum[i][2 * c + 1];
       }
+      if (a.flags & SIMT_EX_KEEP) {
+        if (col < a.M) a.E[row * a.M + col] = err[i][2 * c];
+        if (col + 1 < a.M) a.E[row * a.M + col + 1] = err[i][2 * c + 1];
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- K3 Winograd pair sums, TMA-fed (P even)
-template <class CF, int CV, bool FUSED>
+template <class CF, int CV, bool FUSED, bool EX = false>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(const __grid_constant__ SimtTmaArgs a) {
   using LY = SimtTmaLayout<CF>;
   constexpr int TM = CF::TM, TN = CF::TN;
@@ -211,6 +235,17 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+  if (EX && (a.flags & SIMT_EX_ACC)) {  // continue each entry's pair sum from the previous k-panel
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int64_t row = m0 + simt_row<CF>(ty, i);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t col = n0 + 2 * tx + 2 * CF::TXN * (j / 2) + (j & 1);
+        if (row < a.N && col < a.M) acc[i][j] = a.C[row * a.M + col];
+      }
+    }
+  }
 
 #pragma unroll 1
   for (int kt = 0; kt < pp.KT; ++kt) {
@@ -246,7 +281,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
   for (int i = 0; i < TM; ++i) {
     const int64_t row = m0 + simt_row<CF>(ty, i);
     if (row >= a.N) continue;
-    const double yi = a.y[row];
+    const bool keep = EX && (a.flags & SIMT_EX_KEEP);  // raw pair sums for the next k-panel
+    const double yi = keep ? 0.0 : a.y[row];
 #pragma unroll
     for (int c = 0; c < TN / 2; ++c) {
       const int64_t col = n0 + 2 * tx + 2 * CF::TXN * c;
@@ -254,8 +290,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t cc = col + e;
-        out[e] = cc < a.M ? dsub(dsub(acc[i][2 * c + e], yi), a.z[cc]) : 0.0;  // (acc - y_i) - z_k
-      }
+        out[e] = cc >= a.M ? 0.0 : keep ? acc[i][2 * c + e] : dsub(dsub(acc[i][2 * c + e], yi), a.z[cc]);
+      }  // (acc - y_i) - z_k
       if (CV == 2 && col + 1 < a.M) {
         *reinterpret_cast<double2*>(a.C + row * a.M + col) = make_double2(out[0], out[1]);
       } else {
@@ -282,15 +318,15 @@ inline cudaError_t launch_simt_tma_t_(const SimtTmaArgs& args, unsigned grid, cu
 
 template <class CF>
 inline bool simt_tma_args(SimtTmaArgs& args, const double* A, const double* B, double* C, int64_t N, int64_t P,
-                          int64_t M) {
+                          int64_t M, int64_t lda = 0, int64_t ldb = 0) {
   args.A = A;
   args.B = B;
   args.C = C;
   args.N = N;
   args.P = P;
   args.M = M;
-  return tma_encode_2d(&args.mapA, A, N, P, P, CF::BM, 16, true) &&
-         tma_encode_2d(&args.mapB, B, P, M, M, CF::BK, 16, true);
+  return tma_encode_2d(&args.mapA, A, N, P, lda ? lda : P, CF::BM, 16, true) &&
+         tma_encode_2d(&args.mapB, B, P, M, ldb ? ldb : M, CF::BK, 16, true);
 }
 
 template <class CF, bool FUSED = false>
@@ -317,6 +353,43 @@ inline cudaError_t launch_winograd_pairs_tma(const double* A, const double* B, d
   const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
   return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)
             : launch_simt_tma_t_<winograd_tma_kernel<CF, 1, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st);
+}
+
+// k-panel steps (NEXT-4): A (lda) / B (ldb) are panel views of wider operands, C and E dense N x M
+inline bool simt_tma_ex_ok(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t N, int64_t P,
+                           int64_t M) {
+  return tma_ok(A, lda) && tma_ok(B, ldb) && lda >= P && ldb >= M && M % 2 == 0 && N <= INT32_MAX &&
+         P <= INT32_MAX && M <= INT32_MAX;
+}
+
+template <class CF, bool FUSED>
+inline cudaError_t launch_kahan_tma_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                       double* E, int64_t N, int64_t P, int64_t M, int flags, cudaStream_t st) {
+  using LY = SimtTmaLayout<CF>;
+  SimtTmaArgs args{};
+  if (!simt_tma_args<CF>(args, A, B, C, N, P, M, lda, ldb)) return cudaErrorInvalidValue;
+  args.E = E;
+  args.flags = flags;
+  const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
+  const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+  return cv ? launch_simt_tma_t_<kahan_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<kahan_tma_kernel<CF, 1, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st);
+}
+
+template <class CF, bool FUSED>
+inline cudaError_t launch_winograd_tma_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                          const double* y, const double* z, int64_t N, int64_t P, int64_t M,
+                                          int flags, cudaStream_t st) {
+  using LY = SimtTmaLayout<CF>;
+  SimtTmaArgs args{};
+  if (!simt_tma_args<CF>(args, A, B, C, N, P, M, lda, ldb)) return cudaErrorInvalidValue;
+  args.y = y;
+  args.z = z;
+  args.flags = flags;
+  const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
+  const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+  return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2, FUSED, true>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<winograd_tma_kernel<CF, 1, FUSED, true>, CF::THREADS, LY::SMEM>(args, grid, st);
 }
 
 }  // namespace mmk

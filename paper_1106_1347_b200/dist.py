@@ -11,12 +11,14 @@ no split-K and y_i / z_k are per row / column -- so the classical, Kahan, Winogr
 Winograd shards are bitwise equal to the corresponding rows of the 1-GPU product.  Strassen on
 a shard recurses on (N_local x P x M) and agrees within its tolerance only.
 
-Broadcast/compute overlap, NaivStandard only: with panels > 1, B is
-broadcast as `panels` consecutive row panels (contiguous in memory), all enqueued at once on
-NCCL's stream; the product is accumulated panel by panel with mm_naive_ex(accumulate=1), each
-launch waiting (on the device, not the host) for its own panel only, so the transfer of panel
-i+1 overlaps the DMMA work on panel i.  Because every entry's fma chain continues from C in k
-order (reading R2), the result is bitwise the one-shot product at any panel count.
+Broadcast/compute overlap, NaivStandard, NaivKahan and WinogradOriginal
+(and their fused variants): with panels > 1, B is broadcast as `panels` consecutive row panels
+(contiguous in memory, even boundaries), all enqueued at once on NCCL's stream; the product is
+accumulated panel by panel (mm_naive_ex / mm_kahan_ex / mm_winograd_ex), each launch waiting (on
+the device, not the host) for its own panel only, so the transfer of panel i+1 overlaps the work on
+panel i.  Every entry's running state -- the fma chain (reading R2), Kahan's (sum, err), Winograd's
+pair sum -- continues from panel to panel in k order, so the result is bitwise the one-shot product
+at any panel count; Winograd's y and z are computed from the full operands before the last panel.
 
 The compute and norm callables are injectable so that the host-side logic (sharding, the
 broadcast, the max-reduction and lambda, the panel schedule) is testable with world_size 2 on
@@ -52,10 +54,34 @@ def _default_norm(X):
     return mm.norm_inf(X)
 
 
-def _default_panel(A_panel, B_panel, out, accumulate: bool):
+PANEL_METHODS = ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused")
+
+
+def _default_panel(method, A_panel, B_panel, out, first: bool, last: bool, ctx: dict):
+    """One k-panel step on the GPU.  ctx holds the full operands ("A", "B") and the carried state
+    (Kahan's err "E"; Winograd's "y", "z", computed from the full operands before the last panel)."""
     import paper_1106_1347_b200 as mm
 
-    return mm.naive_panel(A_panel, B_panel, out, accumulate=accumulate)
+    fused = method.endswith("_fused")
+    if method == "naive":
+        return mm.naive_panel(A_panel, B_panel, out, accumulate=not first)
+    if method.startswith("kahan"):
+        if "E" not in ctx:
+            ctx["E"] = torch.empty_like(out)
+        return mm.kahan_panel(A_panel, B_panel, out, ctx["E"], accumulate=not first, keep_state=not last,
+                              fused=fused)
+    y = z = None
+    if last:
+        A, B = ctx["A"], ctx["B"]
+        y = torch.empty(A.shape[0], dtype=torch.float64, device=A.device)
+        z = torch.empty(B.shape[1], dtype=torch.float64, device=B.device)
+        mm.winograd_yz(A, B, y, z, fused=fused)
+    return mm.winograd_panel(A_panel, B_panel, out, y, z, accumulate=not first, keep_state=not last, fused=fused)
+
+
+def panels_supported(method: str, P: int, M: int) -> bool:
+    """NaivStandard always; Kahan / Winograd need the TMA-fed panel kernels: P and M even."""
+    return method == "naive" or (method in PANEL_METHODS and P % 2 == 0 and M % 2 == 0)
 
 
 def panel_bounds(P: int, panels: int):
@@ -66,16 +92,17 @@ def panel_bounds(P: int, panels: int):
     return list(zip(b[:-1], b[1:]))
 
 
-def _dist_naive_panels(A_local, B, out, root, group, panels, panel_compute):
+def _dist_panels(method, A_local, B, out, root, group, panels, panel_compute):
     P, M = B.shape
     bounds = panel_bounds(P, panels)
     works = [dist.broadcast(B[k0:k1], src=root, group=group, async_op=True) for k0, k1 in bounds]
     if out is None:
         out = torch.empty((A_local.shape[0], M), dtype=B.dtype, device=B.device)
+    ctx = {"A": A_local, "B": B}
     for i, (k0, k1) in enumerate(bounds):
         works[i].wait()  # NCCL: the current stream waits for this panel only; gloo: the host waits
         if A_local.shape[0] > 0:
-            panel_compute(A_local[:, k0:k1], B[k0:k1], out, i > 0)
+            panel_compute(method, A_local[:, k0:k1], B[k0:k1], out, i == 0, i == len(bounds) - 1, ctx)
     return out
 
 
@@ -85,12 +112,14 @@ def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optio
               panel_compute: Optional[Callable] = None) -> torch.Tensor:
     """C_local = A_local B on every rank.  B must be allocated (P x M) on every rank; its content
     on `root` is broadcast (in place) before / during the product.  A rank with no rows still
-    takes part in the collectives and returns an empty (0 x M) result.  panels > 1 (method
-    "naive" only): panelised broadcast overlapped with the accumulation (NEXT-4)."""
+    takes part in the collectives and returns an empty (0 x M) result.  panels > 1 (NaivStandard;
+    NaivKahan / WinogradOriginal and the fused variants when P and M are even): panelised broadcast
+    overlapped with the accumulation (NEXT-4); panel_compute(method, A_panel, B_panel, out, first,
+    last, ctx) performs one panel step."""
     compute = compute or _default_compute
     norm = norm or _default_norm
-    if method == "naive" and panels > 1:
-        return _dist_naive_panels(A_local, B, out, root, group, panels, panel_compute or _default_panel)
+    if panels > 1 and panels_supported(method, B.shape[0], B.shape[1]):
+        return _dist_panels(method, A_local, B, out, root, group, panels, panel_compute or _default_panel)
     dist.broadcast(B, src=root, group=group)
     norms = None
     if method == "winograd_scaled":

@@ -30,8 +30,12 @@ def _oracle_compute(method, A, B, out, levels, norms):
         C = oracle.naive_fma(A_np, B_np)
     elif method == "kahan":
         C = oracle.naive_kahan(A_np, B_np)
+    elif method == "kahan_fused":
+        C = oracle.naive_kahan_fused(A_np, B_np)
     elif method == "winograd":
         C = oracle.winograd_original(A_np, B_np)
+    elif method == "winograd_fused":
+        C = oracle.winograd_fused(A_np, B_np)
     elif method == "winograd_scaled":
         lam = oracle.lam(float(norms[0]), float(norms[1]))
         idx = [(i, j) for i in range(A_np.shape[0]) for j in range(B_np.shape[1])]
@@ -41,13 +45,28 @@ def _oracle_compute(method, A, B, out, levels, norms):
     return torch.from_numpy(C)
 
 
-def _oracle_panel(A_panel, B_panel, out, accumulate):
+def _oracle_panel(method, A_panel, B_panel, out, first, last, ctx):
+    """The panel step of each method through the oracle's resumable loops (state kept in `out`
+    and ctx); the last Winograd panel applies the epilogue with y, z of the full operands."""
     import oracle
 
     C = out.numpy()
-    if not accumulate:
+    fused = method.endswith("_fused")
+    Ap, Bp = A_panel.numpy(), B_panel.numpy()
+    if first:
         C[...] = 0.0
-    oracle.naive_fma_acc(A_panel.numpy(), B_panel.numpy(), C)
+    if method == "naive":
+        oracle.naive_fma_acc(Ap, Bp, C)
+    elif method.startswith("kahan"):
+        if first:
+            ctx["E"] = np.zeros_like(C)
+        oracle.naive_kahan_acc(Ap, Bp, C, ctx["E"], fused)
+    else:
+        oracle.winograd_pairs_acc(Ap, Bp, C, fused)
+        if last:
+            A, B = ctx["A"].numpy(), ctx["B"].numpy()
+            y, z = oracle.winograd_yz_fused(A, B) if fused else oracle.winograd_yz(A, B)
+            C[...] = oracle.winograd_finish(C, y, z)
     return out
 
 
@@ -79,12 +98,14 @@ def _worker(rank, world, port, N, P, M, seed, q):
             C = dist_gemm(m, A_loc, Bt, compute=_oracle_compute, norm=_oracle_norm)
             out[m] = C.numpy().copy()
         assert np.array_equal(Bt.numpy(), B)  # broadcast delivered B everywhere
-        # NEXT-4: panelised broadcast + chain-continuing accumulation, B re-broadcast from scratch
+        # NEXT-4: panelised broadcast + state-continuing accumulation, B re-broadcast from scratch
+        # (Kahan / Winograd take the panel path only for even P and M, else the one-shot compute)
         for panels in (2, 3, 5):
-            Bp = torch.from_numpy(B.copy()) if rank == 0 else torch.full((P, M), np.nan, dtype=torch.float64)
-            C = dist_gemm("naive", A_loc, Bp, panels=panels, panel_compute=_oracle_panel)
-            assert np.array_equal(Bp.numpy(), B)
-            out[f"naive_p{panels}"] = C.numpy().copy()
+            for m in ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused"):
+                Bp = torch.from_numpy(B.copy()) if rank == 0 else torch.full((P, M), np.nan, dtype=torch.float64)
+                C = dist_gemm(m, A_loc, Bp, panels=panels, panel_compute=_oracle_panel, compute=_oracle_compute)
+                assert np.array_equal(Bp.numpy(), B)
+                out[f"{m}_p{panels}"] = C.numpy().copy()
         q.put((rank, lo, hi, out))
     finally:
         dist.destroy_process_group()
@@ -116,7 +137,7 @@ def _run(world, N, P, M, seed):
     return sorted(res, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16)])
+@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16), (7, 20, 10)])
 def test_row_sharded_bitwise(shape):
     import oracle
     import workload
@@ -128,7 +149,9 @@ def test_row_sharded_bitwise(shape):
     full = {
         "naive": oracle.naive_fma(A, B),
         "kahan": oracle.naive_kahan(A, B),
+        "kahan_fused": oracle.naive_kahan_fused(A, B),
         "winograd": oracle.winograd_original(A, B),
+        "winograd_fused": oracle.winograd_fused(A, B),
         "winograd_scaled": oracle.winograd_scaled(A, B)[0],
     }
     assert oracle.winograd_scaled(A, B)[1] != 0

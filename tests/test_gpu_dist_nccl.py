@@ -28,14 +28,23 @@ SCRIPT = textwrap.dedent(r"""
     A, B = workload.custom(700, 1024, 520, seed=3)
     dA = torch.from_numpy(A * 1e3).to(dev)
     hB = torch.from_numpy(B).to(dev)
-    for m in ("naive", "kahan", "winograd", "winograd_scaled", "strassen", "strassen_winograd"):
+    for m in ("naive", "kahan", "winograd", "winograd_scaled", "strassen", "strassen_winograd", "kahan_fused",
+              "winograd_fused"):
         kw = {"levels": 2} if m.startswith("strassen") else {}
         ref = getattr(mm, m)(dA, hB, **kw)
-        for panels in (1, 4):
+        for panels in (1, 4, 7):
             Bw = hB.clone()
             C = dist_gemm(m, dA, Bw, levels=2, panels=panels)
             torch.cuda.synchronize()
             assert torch.equal(C, ref), (m, panels)
+    # odd P: Kahan / Winograd fall back to one broadcast + the one-shot kernel (cp.async paths)
+    A3, B3 = workload.custom(300, 1001, 260, seed=4)
+    dA3, hB3 = torch.from_numpy(A3).to(dev), torch.from_numpy(B3).to(dev)
+    for m in ("naive", "kahan", "winograd"):
+        ref = getattr(mm, m)(dA3, hB3)
+        C = dist_gemm(m, dA3, hB3.clone(), panels=4)
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref), ("odd P", m)
     # the C ABI's own layer (mm_dist_*): NCCL driven from libmm_b200.so
     from paper_1106_1347_b200.dist import NativeComm
     comm = NativeComm()
@@ -49,6 +58,11 @@ SCRIPT = textwrap.dedent(r"""
             torch.cuda.synchronize()
             assert torch.equal(C, ref), ("native", m, panels)
             assert torch.equal(Bw, hB)
+    for m in ("naive", "kahan", "winograd", "kahan_fused", "winograd_fused"):
+        ref = getattr(mm, m)(dA3, hB3)
+        C = comm.gemm(m, dA3, hB3.clone(), panels=5)
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref), ("native odd P", m)
     # a rank without rows still takes part (the product is empty)
     C0 = comm.gemm("winograd_scaled", dA[:0], hB.clone())
     torch.cuda.synchronize()

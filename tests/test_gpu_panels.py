@@ -45,3 +45,67 @@ def test_accumulate_matches_oracle_strided():
     got = dC.cpu().numpy()
     assert np.array_equal(got[:, 3:47], ref)
     assert np.all(got[:, :3] == 0) and np.all(got[:, 47:] == 0)  # nothing outside the view is touched
+
+
+# ---- NaivKahan / WinogradOriginal k-panels (mm_kahan_ex / mm_winograd_ex, NEXT-4) ----------
+PANEL_CASES = [((300, 1000, 260), [2, 500, 998]), ((333, 130, 66), [64, 66]), ((2210, 1002, 1094), [96, 502]),
+               ((40, 8, 2), [2, 4, 6])]
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("shape,cuts", PANEL_CASES)
+def test_kahan_panels_compose_bitwise(shape, cuts, fused):
+    """(sum, err) carried from panel to panel in C and E: bitwise the one-shot NaivKahan."""
+    N, P, M = shape
+    A, B = workload.custom(N, P, M, seed=N + 3 * P + M)
+    A = A * 1e4
+    dA, dB = dev(A), dev(B)
+    full = (mm.kahan_fused if fused else mm.kahan)(dA, dB).cpu().numpy()
+    C = torch.empty((N, M), dtype=torch.float64, device=DEV)
+    E = torch.empty((N, M), dtype=torch.float64, device=DEV)
+    b = [0] + cuts + [P]
+    for i, (k0, k1) in enumerate(zip(b[:-1], b[1:])):
+        mm.kahan_panel(dA[:, k0:k1], dB[k0:k1], C, E, accumulate=i > 0, keep_state=k1 < P, fused=fused)
+    assert np.array_equal(C.cpu().numpy(), full)
+    if N * P * M <= 300 * 1000 * 260:
+        ref = oracle.naive_kahan_fused(A, B) if fused else oracle.naive_kahan(A, B)
+        assert np.array_equal(full, ref)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("shape,cuts", PANEL_CASES)
+def test_winograd_panels_compose_bitwise(shape, cuts, fused):
+    """Raw pair sums carried in C from panel to panel, y / z of the full operands applied by the
+    last panel: bitwise the one-shot WinogradOriginal."""
+    N, P, M = shape
+    A, B = workload.custom(N, P, M, seed=N + 5 * P + M)
+    dA, dB = dev(A), dev(B)
+    full = (mm.winograd_fused if fused else mm.winograd)(dA, dB).cpu().numpy()
+    y = torch.empty(N, dtype=torch.float64, device=DEV)
+    z = torch.empty(M, dtype=torch.float64, device=DEV)
+    mm.winograd_yz(dA, dB, y, z, fused=fused)
+    C = torch.empty((N, M), dtype=torch.float64, device=DEV)
+    b = [0] + cuts + [P]
+    for i, (k0, k1) in enumerate(zip(b[:-1], b[1:])):
+        mm.winograd_panel(dA[:, k0:k1], dB[k0:k1], C, y, z, accumulate=i > 0, keep_state=k1 < P, fused=fused)
+    assert np.array_equal(C.cpu().numpy(), full)
+    if N * P * M <= 300 * 1000 * 260:
+        ref = oracle.winograd_fused(A, B) if fused else oracle.winograd_original(A, B)
+        assert np.array_equal(full, ref)
+
+
+def test_panel_ex_argument_errors():
+    L = mm.lib()
+    A = torch.zeros((8, 10), dtype=torch.float64, device=DEV)
+    B = torch.zeros((10, 6), dtype=torch.float64, device=DEV)
+    C = torch.zeros((8, 6), dtype=torch.float64, device=DEV)
+    E = torch.zeros((8, 6), dtype=torch.float64, device=DEV)
+    p = lambda t: t.data_ptr()  # noqa: E731
+    assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), None, 8, 10, 6, 1, None) == -1      # ACCUMULATE needs E
+    assert L.mm_kahan_ex(p(A) + 8, 10, p(B), 6, p(C), p(E), 8, 9, 6, 0, None) == -1  # A not 16-byte aligned
+    assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), p(E), 8, 10, 6, 8, None) == -1     # unknown flag
+    assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(A), p(E), 8, 10, 6, 0, None) == -2     # C aliases A
+    assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), p(C), 8, 10, 6, 2, None) == -2     # E aliases C
+    assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 9, 6, 2, None) == -1  # odd panel width
+    assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 10, 6, 0, None) == -1  # epilogue needs y, z
+    assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), p(E), 8, 10, 6, 2, None) == 0
