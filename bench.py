@@ -58,7 +58,9 @@ def parse_args():
     ap.add_argument("--levels", type=int, default=3, help="Strassen recursion levels (c4: 3 levels, 1024^3 leaves, is fastest: profiles/r01/table_v2.jsonl)")
     ap.add_argument("--methods", default=",".join(METHODS))
     ap.add_argument("--panels", type=int, default=8,
-                    help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation")
+                    help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation "
+                         "(NaivKahan / WinogradOriginal: half as many; their per-panel cost is higher, "
+                         "profiles/r01/panel_bench.jsonl)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="N > 1 collectives (gloo only to exercise the multi-rank path on fewer GPUs)")
     ap.add_argument("--e2e-blocks", type=int, default=8,
@@ -212,7 +214,8 @@ def config_dict(args, cfg, world):
         "workload": f"{cfg.key}: A {cfg.N}x{cfg.P}, B {cfg.P}x{cfg.M} float64 ({cfg.dist}), one call of each of "
                     f"{args.methods.replace(',', ', ')} per step",
         "N": cfg.N, "P": cfg.P, "M": cfg.M, "strassen_levels": args.levels,
-        "parallelism": (f"row-block dp{world} (B broadcast via {args.dist_backend}; naive: {args.panels} k-panels overlapped)"
+        "parallelism": (f"row-block dp{world} (B broadcast via {args.dist_backend}; k-panels overlapped: naive "
+                        f"{args.panels}, kahan / winograd {max(1, args.panels // 2)})"
                         if world > 1 else "1 GPU"),
         "l2": "inputs larger than L2 (A, B, C = 537 MB each vs 126 MB L2)" if cfg.N >= 4096
         else "inputs smaller than L2 (not flushed)",
@@ -253,11 +256,14 @@ def run_mine(args):
     # N > 1 over NCCL: the C ABI's own layer (mm_dist_*); over gloo: the torch.distributed driver
     native = mmdist.NativeComm() if world > 1 and args.dist_backend == "nccl" else None
 
+    def panels_for(m):
+        return args.panels if m == "naive" else max(1, args.panels // 2)
+
     def one_method(m):
         if native is not None:
-            return native.gemm(m, A, B, out=outs[m], levels=args.levels, panels=args.panels)
+            return native.gemm(m, A, B, out=outs[m], levels=args.levels, panels=panels_for(m))
         if world > 1:
-            return mmdist.dist_gemm(m, A, B, out=outs[m], levels=args.levels, panels=args.panels)
+            return mmdist.dist_gemm(m, A, B, out=outs[m], levels=args.levels, panels=panels_for(m))
         if m == "winograd_scaled":
             return mm.winograd_scaled(A, B, out=outs[m])
         if m in ("strassen", "strassen_winograd"):
@@ -413,10 +419,11 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
         if rank == 0:
             dB.copy_(hB, non_blocking=True)
         for m in methods:
+            pn = args.panels if m == "naive" else max(1, args.panels // 2)
             if native is not None:
-                C = native.gemm(m, dA, dB, levels=args.levels, panels=args.panels)
+                C = native.gemm(m, dA, dB, levels=args.levels, panels=pn)
             else:
-                C = mmdist.dist_gemm(m, dA, dB, levels=args.levels, panels=args.panels)
+                C = mmdist.dist_gemm(m, dA, dB, levels=args.levels, panels=pn)
             hC.copy_(C, non_blocking=True)
         stream.synchronize()
 
