@@ -455,16 +455,57 @@ def _h2d_2d(dA: torch.Tensor, hA: torch.Tensor, k0: int, k1: int, stream) -> Non
         raise MMError(f"cudaMemcpy2DAsync failed: {err}")
 
 
+def _growing_panels(P: int, n: int, ratio: float = 1.4):
+    """n consecutive k-panels of P with even boundaries whose widths grow by `ratio`: the first
+    panel's host->device copy is all the product waits for, and each later copy (A's columns and
+    B's rows, ~2.6 us per k at c4 over PCIe) hides under the previous panel's DMMA work (~3.7 us
+    per k), which grows ~1.4x faster than the copy."""
+    n = max(1, min(n, P // 2 if P >= 2 else 1))
+    w = [ratio ** i for i in range(n)]
+    tot = sum(w)
+    cuts, acc = [], 0.0
+    for x in w[:-1]:
+        acc += x
+        c = 2 * int(round(P * acc / tot / 2))
+        if (not cuts or c > cuts[-1]) and 0 < c < P:
+            cuts.append(c)
+    b = [0] + cuts + [P]
+    return list(zip(b[:-1], b[1:]))
+
+
+def _shrinking_rows(N: int, n: int, quantum: int = 64, min_rows: int = 1024):
+    """At most n row blocks of N halving in size (multiples of `quantum` rows, the SIMT kernels'
+    tile height; none below `min_rows`, which still fills the GPU): the device->host copy of every
+    block but the last hides under the next block's kernel, and the last block -- the only copy
+    left after the final kernel -- is small.  min_rows = 1024: blocks of a few waves lose more to
+    their partial last wave than the smaller final copy saves (profiles/r01/e2e_schedule.jsonl)."""
+    if n <= 1 or N < 2 * min_rows:
+        return [(0, N)]
+    sizes, rest = [], N
+    for _ in range(n - 1):
+        sz = max(quantum, (rest // 2) // quantum * quantum)
+        if rest - sz < min_rows:
+            break
+        sizes.append(sz)
+        rest -= sz
+    sizes.append(rest)
+    b = [0]
+    for sz in sizes:
+        b.append(b[-1] + sz)
+    return list(zip(b[:-1], b[1:]))
+
+
 def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2, device=None,
                    outs: Optional[dict] = None, row_blocks: int = 4) -> dict:
     """The shape of the paper's test program: several methods applied to the
     SAME host operands.  A and B (pinned host float64) are copied to the device once; every
     method's product is copied back into outs[method] (pinned host, allocated if missing) on a
     copy stream while the next method computes.  When the first method is NaivStandard, A and B
-    travel in k-panels (A's column panels as 2-D copies) and the product accumulates panel by
-    panel as they land (mm_naive_ex, reading R23: bitwise the one-shot chain); when it is another
-    row-local method its row blocks start as soon as their rows of A have landed.  When the last
-    method is row-local its result streams back by row blocks.  Each product is bitwise the
+    travel in k-panels of growing width (A's column panels as 2-D copies) and the product
+    accumulates panel by panel as they land (mm_naive_ex, reading R23: bitwise the one-shot
+    chain); when it is another row-local method its row blocks start as soon as their rows of A
+    have landed.  When the last method is row-local its result streams back by row blocks of
+    shrinking height.  Each product is bitwise the
     one-shot device call's."""
     methods = list(methods)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -480,9 +521,8 @@ def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2
     bounds = [(N * b) // rb for b in range(rb + 1)]
     k_panels = None
     if methods and methods[0] == "naive" and A.is_pinned() and B.is_pinned() and A.is_contiguous() and P >= 4:
-        from .dist import panel_bounds
-
-        k_panels = panel_bounds(P, row_blocks)
+        k_panels = _growing_panels(P, row_blocks)
+    tail = _shrinking_rows(N, row_blocks)  # the last method's row blocks (see below)
     s_in.wait_stream(s)
     with torch.cuda.stream(s_in):
         dA = torch.empty((N, P), dtype=torch.float64, device=dev)
@@ -521,10 +561,17 @@ def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2
             s_out.wait_stream(s)
             with torch.cuda.stream(s_out):
                 outs[m].copy_(buf, non_blocking=True)
-        elif row_local and (first or last):
+        elif row_local and first:  # its row blocks start as their rows of A land
             for b in range(rb):
                 lo, hi = bounds[b], bounds[b + 1]
                 s.wait_event(a_ready[b] if k_panels is None else a_ready[-1])
+                f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
+                s_out.wait_stream(s)
+                with torch.cuda.stream(s_out):
+                    outs[m][lo:hi].copy_(buf[lo:hi], non_blocking=True)
+        elif row_local and last:  # shrinking row blocks: only the small last block's copy is exposed
+            s.wait_event(a_ready[-1])
+            for lo, hi in tail:
                 f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
                 s_out.wait_stream(s)
                 with torch.cuda.stream(s_out):
