@@ -384,18 +384,20 @@ def test_norm_inf_many_shapes():
 def test_matmul_methods_bitwise():
     """matmul_methods (the paper's test-program shape: every method on the same host operands,
     copies overlapped with the kernels) gives every method's one-shot device result bit for bit."""
-    A, B = workload.custom(517, 130, 258, seed=12)
-    hA = torch.from_numpy(A).pin_memory()
-    hB = torch.from_numpy(B).pin_memory()
-    dA, dB = dev(A), dev(B)
-    # naive first: k-panel pipeline (2-D copies of A's column panels + accumulate-mode GEMM);
-    # kahan first: row-block pipeline; a row-local method last: row-block D2H
-    for order in (["naive", "strassen", "winograd_scaled", "winograd", "kahan"],
-                  ["kahan", "strassen_winograd", "naive"]):
-        outs = mm.matmul_methods(hA, hB, order, levels=1)
-        for m in order:
-            ref = host(run(m, dA, dB, 1))
-            assert np.array_equal(outs[m].numpy(), ref), (order, m)
+    # naive first: growing k-panels (2-D copies of A's column panels + accumulate-mode GEMM);
+    # kahan first: row-block pipeline; a row-local method last: shrinking row-block D2H (N = 2500
+    # gives it two blocks, 1216 + 1284 rows; N = 517 one)
+    for shape in ((517, 130, 258), (2500, 202, 330)):
+        A, B = workload.custom(*shape, seed=12)
+        hA = torch.from_numpy(A).pin_memory()
+        hB = torch.from_numpy(B).pin_memory()
+        dA, dB = dev(A), dev(B)
+        for order in (["naive", "strassen", "winograd_scaled", "winograd", "kahan"],
+                      ["kahan", "strassen_winograd", "naive"], ["naive", "winograd"]):
+            outs = mm.matmul_methods(hA, hB, order, levels=1)
+            for m in order:
+                ref = host(run(m, dA, dB, 1))
+                assert np.array_equal(outs[m].numpy(), ref), (shape, order, m)
 
 
 @pytest.mark.parametrize("method", ["strassen", "strassen_winograd"])
