@@ -151,6 +151,8 @@ int main(int argc, char** argv) {
     kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_2cta_bk32", c);
     kahan_tma<SimtCfg<64, 64, 4, 8, 2, 3, 32>>("tma_64x64_s2_3cta_bk32", c);
     kahan_tma<SimtCfg<64, 64, 4, 8, 4, 3, 16>>("tma_64x64_s4_3cta_bk16", c);
+    kahan_tma<SimtCfg<48, 64, 3, 8, 4, 3, 16>>("tma_48x64_t3x8_s4_3cta_bk16", c);
+    kahan_tma<SimtCfg<48, 64, 3, 8, 2, 3, 32>>("tma_48x64_t3x8_s2_3cta_bk32", c);
     return 0;
   }
   if (wino_only) {  // K3 configurations only
@@ -161,6 +163,8 @@ int main(int argc, char** argv) {
     wino_tma<SimtCfg<64, 64, 4, 8, 3, 3, 32>>("tma_64x64_t4x8_s3_3cta_bk32", c);
     wino_tma<SimtCfg<128, 64, 8, 8, 2, 3, 16>>("tma_128x64_s2_3cta_bk16", c);
     wino_tma<SimtCfg<128, 64, 8, 8, 3, 3, 16>>("tma_128x64_s3_3cta_bk16", c);
+    wino_tma<SimtCfg<96, 64, 6, 8, 3, 3, 16>>("tma_96x64_t6x8_s3_3cta_bk16", c);
+    wino_tma<SimtCfg<96, 64, 6, 8, 2, 3, 16>>("tma_96x64_t6x8_s2_3cta_bk16", c);
     return 0;
   }
   kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
