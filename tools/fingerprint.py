@@ -37,16 +37,23 @@ def run():
     torch.cuda.synchronize()
 
 
+def _fused(kernel: str) -> bool:
+    """The FUSED template argument: the one after CV in <SimtCfg<...>, CV, FUSED[, EX]>."""
+    tail = kernel[kernel.index(">") + 1:].strip(" ,>")
+    args = [t.strip() for t in tail.split(",") if t.strip()]
+    return len(args) >= 2 and args[1] in ("1", "true")
+
+
 def expected(kernel: str):
     n3, n2 = N ** 3, N ** 2
     half = n3 // 2
     if kernel.startswith("dgemm"):
         return None  # batched Strassen leaves share the kernel; see the DMMA ratio column
-    if kernel.startswith(("kahan_gemm_kernel", "kahan_tma_kernel")) and kernel.rstrip(">").endswith("1"):
+    if kernel.startswith(("kahan_gemm_kernel", "kahan_tma_kernel")) and _fused(kernel):
         return {"dadd": 3 * n3, "dmul": 0, "dfma": n3, "dmma": 0}
     if kernel.startswith(("kahan_gemm_kernel", "kahan_tma_kernel")):
         return {"dadd": 4 * n3, "dmul": n3, "dfma": 0, "dmma": 0}
-    if kernel.startswith("winograd_tma_kernel") and kernel.rstrip(">").endswith("1"):
+    if kernel.startswith("winograd_tma_kernel") and _fused(kernel):
         return {"dadd": 2 * half + 2 * n2, "dmul": 0, "dfma": half, "dmma": 0}
     if kernel.startswith("winograd_tma_kernel"):
         return {"dadd": 3 * half + 2 * n2, "dmul": half, "dfma": 0, "dmma": 0}
