@@ -93,6 +93,10 @@ int main(int argc, char** argv) {
     fill<<<1024, 256>>>(B, 1002 * 3000, 2);
     run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 32, 2, 1, 4, 6>, false>("cpasync_64x32_w2x1_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<32, 64, 1, 2, 4, 6>, false>("cpasync_32x64_w1x2_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 4>, false>("cpasync_64x64_s3_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 4, 32>, false>("cpasync_64x64_bk32_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P1000", A, B, C, 4096, 1000, 3000, 20);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_P1000", A, B, C, 4096, 1000, 3000, 20);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 3>, true>("tma_64x64_P1002", A, B, C, 4096, 1002, 3000, 20);
