@@ -109,3 +109,39 @@ def test_panel_ex_argument_errors():
     assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 9, 6, 2, None) == -1  # odd panel width
     assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 10, 6, 0, None) == -1  # epilogue needs y, z
     assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), p(E), 8, 10, 6, 2, None) == 0
+
+
+def test_random_panel_splits_all_row_local_methods():
+    """Seeded random k-splits (even cut points, 1-6 panels) of ragged TMA-path problems: every
+    row-local method's panel composition is bitwise its one-shot product."""
+    rng = np.random.default_rng(2024)
+    for trial in range(12):
+        N = int(rng.integers(1, 700))
+        P = 2 * int(rng.integers(1, 400))
+        M = 2 * int(rng.integers(1, 300))
+        A, B = workload.custom(N, P, M, seed=7000 + trial)
+        A = A * 10.0 ** rng.integers(-3, 4)
+        dA, dB = dev(A), dev(B)
+        ncut = int(rng.integers(0, min(5, P // 2 - 1) + 1)) if P > 2 else 0
+        cuts = sorted(set((2 * rng.integers(1, P // 2, size=ncut)).tolist())) if ncut else []
+        b = [0] + cuts + [P]
+        C = torch.empty((N, M), dtype=torch.float64, device=DEV)
+        E = torch.empty((N, M), dtype=torch.float64, device=DEV)
+        y = torch.empty(N, dtype=torch.float64, device=DEV)
+        z = torch.empty(M, dtype=torch.float64, device=DEV)
+        for name in ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused"):
+            fused = name.endswith("_fused")
+            if name.startswith("winograd"):
+                mm.winograd_yz(dA, dB, y, z, fused=fused)
+            for i, (k0, k1) in enumerate(zip(b[:-1], b[1:])):
+                first, last = i == 0, k1 == P
+                if name == "naive":
+                    mm.naive_panel(dA[:, k0:k1], dB[k0:k1], C, accumulate=not first)
+                elif name.startswith("kahan"):
+                    mm.kahan_panel(dA[:, k0:k1], dB[k0:k1], C, E, accumulate=not first, keep_state=not last,
+                                   fused=fused)
+                else:
+                    mm.winograd_panel(dA[:, k0:k1], dB[k0:k1], C, y, z, accumulate=not first, keep_state=not last,
+                                      fused=fused)
+            full = getattr(mm, name)(dA, dB)
+            assert torch.equal(C, full), (trial, (N, P, M), b, name)
