@@ -14,6 +14,9 @@
 //    the four C quadrants (P:279-282 / P:307-311, left to right as displayed); at level 0
 //    it writes straight into the caller's C, dropping the padding (the "extract" of P:286).
 // All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
+//  * two levels per pass (strassen_form2_kernel / strassen_combine2_kernel) for the deepest
+//    pairs of levels: the intermediate level -- 7/4 the data of the one above it -- is never
+//    written nor re-read (c4, d = 3: 24.6 -> 23.0 ms per product).
 #pragma once
 #include "common.cuh"
 #include "gemm_tma.cuh"
@@ -77,6 +80,69 @@ __device__ __forceinline__ void ld_quad(const FormArgs& a, const double* base, i
 // so every warp access is a contiguous, fully used run of sectors), 256 >> TPRS row units per
 // block, grid-stride over all cnt * h_rows units.  Index arithmetic is once per row unit.
 
+// the seven child operands of one node at one element position, from its four quadrants'
+// values: P:271-277 (StrassenNaiv) / P:300-306 (StrassenWinograd), the oracle's operations in
+// the oracle's order
+template <int VARIANT, int SIDE>
+__device__ __forceinline__ void form7(double x11, double x12, double x21, double x22, double (&o)[7]) {
+  if (VARIANT == SV_NAIV) {
+    if (SIDE == 0) {              // P:271-277, left factors
+      o[0] = dadd(x11, x22);  // H1: A11 + A22
+      o[1] = dadd(x21, x22);  // H2: A21 + A22
+      o[2] = x11;             // H3: A11
+      o[3] = x22;             // H4: A22
+      o[4] = dadd(x11, x12);  // H5: A11 + A12
+      o[5] = dsub(x21, x11);  // H6: A21 - A11
+      o[6] = dsub(x12, x22);  // H7: A12 - A22
+    } else {                      // right factors
+      o[0] = dadd(x11, x22);  // H1: B11 + B22
+      o[1] = x11;             // H2: B11
+      o[2] = dsub(x12, x22);  // H3: B12 - B22
+      o[3] = dsub(x21, x11);  // H4: B21 - B11
+      o[4] = x22;             // H5: B22
+      o[5] = dadd(x11, x12);  // H6: B11 + B12
+      o[6] = dadd(x21, x22);  // H7: B21 + B22
+    }
+  } else {
+    if (SIDE == 0) {
+      const double a1 = dsub(x11, x21);  // A1 = A11 - A21
+      const double a2 = dsub(x22, a1);   // A2 = A22 - A1
+      o[0] = x11;                        // H1: A11
+      o[1] = x12;                        // H2: A12
+      o[2] = a2;                         // H3: A2
+      o[3] = dadd(x21, x22);             // H4: A21 + A22
+      o[4] = a1;                         // H5: A1
+      o[5] = dsub(x12, a2);              // H6: A12 - A2
+      o[6] = x22;                        // H7: A22
+    } else {
+      const double b1 = dsub(x22, x12);  // B1 = B22 - B12
+      const double b2 = dadd(b1, x11);   // B2 = B1 + B11
+      o[0] = x11;                        // H1: B11
+      o[1] = x21;                        // H2: B21
+      o[2] = b2;                         // H3: B2
+      o[3] = dsub(x12, x11);             // H4: B12 - B11
+      o[4] = b1;                         // H5: B1
+      o[5] = x22;                        // H6: B22
+      o[6] = dsub(x21, b2);              // H7: B21 - B2
+    }
+  }
+}
+
+// child c alone (c warp-uniform): the same operations as form7's c-th output
+template <int VARIANT, int SIDE>
+__device__ __forceinline__ double form1(int c, double x11, double x12, double x21, double x22) {
+  double o[7];
+  switch (c) {  // each case evaluates only what form7 does for output c
+    case 0: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[0]; }
+    case 1: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[1]; }
+    case 2: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[2]; }
+    case 3: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[3]; }
+    case 4: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[4]; }
+    case 5: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[5]; }
+    default: { form7<VARIANT, SIDE>(x11, x12, x21, x22, o); return o[6]; }
+  }
+}
+
 // SIDE 0 = left operands (from A), SIDE 1 = right operands (from B)
 template <int VARIANT, int SIDE, int V>
 __global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a, int tprs) {
@@ -97,50 +163,67 @@ __global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a, int tprs
       double o[7][V];
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        if (VARIANT == SV_NAIV) {
-          if (SIDE == 0) {              // P:271-277, left factors
-            o[0][e] = dadd(x11[e], x22[e]);  // H1: A11 + A22
-            o[1][e] = dadd(x21[e], x22[e]);  // H2: A21 + A22
-            o[2][e] = x11[e];                // H3: A11
-            o[3][e] = x22[e];                // H4: A22
-            o[4][e] = dadd(x11[e], x12[e]);  // H5: A11 + A12
-            o[5][e] = dsub(x21[e], x11[e]);  // H6: A21 - A11
-            o[6][e] = dsub(x12[e], x22[e]);  // H7: A12 - A22
-          } else {                      // right factors
-            o[0][e] = dadd(x11[e], x22[e]);  // H1: B11 + B22
-            o[1][e] = x11[e];                // H2: B11
-            o[2][e] = dsub(x12[e], x22[e]);  // H3: B12 - B22
-            o[3][e] = dsub(x21[e], x11[e]);  // H4: B21 - B11
-            o[4][e] = x22[e];                // H5: B22
-            o[5][e] = dadd(x11[e], x12[e]);  // H6: B11 + B12
-            o[6][e] = dadd(x21[e], x22[e]);  // H7: B21 + B22
-          }
-        } else {
-          if (SIDE == 0) {
-            const double a1 = dsub(x11[e], x21[e]);  // A1 = A11 - A21
-            const double a2 = dsub(x22[e], a1);      // A2 = A22 - A1
-            o[0][e] = x11[e];                        // H1: A11
-            o[1][e] = x12[e];                        // H2: A12
-            o[2][e] = a2;                            // H3: A2
-            o[3][e] = dadd(x21[e], x22[e]);          // H4: A21 + A22
-            o[4][e] = a1;                            // H5: A1
-            o[5][e] = dsub(x12[e], a2);              // H6: A12 - A2
-            o[6][e] = x22[e];                        // H7: A22
-          } else {
-            const double b1 = dsub(x22[e], x12[e]);  // B1 = B22 - B12
-            const double b2 = dadd(b1, x11[e]);      // B2 = B1 + B11
-            o[0][e] = x11[e];                        // H1: B11
-            o[1][e] = x21[e];                        // H2: B21
-            o[2][e] = b2;                            // H3: B2
-            o[3][e] = dsub(x12[e], x11[e]);          // H4: B12 - B11
-            o[4][e] = b1;                            // H5: B1
-            o[5][e] = x22[e];                        // H6: B22
-            o[6][e] = dsub(x21[e], b2);              // H7: B21 - B2
-          }
-        }
+        double r7[7];
+        form7<VARIANT, SIDE>(x11[e], x12[e], x21[e], x22[e], r7);
+#pragma unroll
+        for (int t = 0; t < 7; ++t) o[t][e] = r7[t];
       }
 #pragma unroll
       for (int t = 0; t < 7; ++t) stv<V>(d0 + t * child_elems + j, o[t]);
+    }
+  }
+}
+
+// Two recursion levels in one pass (l -> l + 2): each thread reads the 16 sub-blocks' values of
+// a node at one position, forms its 7 children's 4 quadrant values (form7 per quadrant) and
+// from those the 49 grandchildren -- the same per-element operations and order as two
+// single-level passes (bitwise the same operands), without writing and re-reading level l + 1
+// (the deepest two levels carry most of the formation traffic: 7/4 more data per level).
+// FormArgs: h_rows / h_cols are the GRANDCHILD dims (a quarter of the parent's), dst holds
+// 49 cnt nodes.
+template <int VARIANT, int SIDE, int V>
+__global__ void __launch_bounds__(256) strassen_form2_kernel(FormArgs a, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
+  const int64_t units = a.cnt * a.h_rows;
+  const int64_t gelems = a.h_rows * a.h_cols;
+  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* base = a.src + q * a.src_stride;
+    double* d0 = a.dst + (49 * q) * gelems + i * a.h_cols;
+    for (int64_t j = int64_t(lt) * V; j < a.h_cols; j += step) {
+      double x[4][4][V];  // x[row sub-block][col sub-block]
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+        for (int pc = 0; pc < 4; ++pc) ld_quad<V>(a, base, i + pr * a.h_rows, j + pc * a.h_cols, x[pr][pc]);
+      // child c (a warp-uniform loop, not unrolled: keeps the register count low enough for
+      // two blocks per SM), its quadrant (qa, qb) = child c of the parent quadrants' (qa, qb)
+      // sub-blocks, then its 7 children
+      double* p = d0 + j;
+#pragma unroll 1
+      for (int c = 0; c < 7; ++c) {
+        double g[7][V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          double cq[2][2];
+#pragma unroll
+          for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb)
+              cq[qa][qb] = form1<VARIANT, SIDE>(c, x[qa][qb][e], x[qa][2 + qb][e], x[2 + qa][qb][e],
+                                                x[2 + qa][2 + qb][e]);
+          double r7[7];
+          form7<VARIANT, SIDE>(cq[0][0], cq[0][1], cq[1][0], cq[1][1], r7);
+#pragma unroll
+          for (int t = 0; t < 7; ++t) g[t][e] = r7[t];
+        }
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+          stv<V>(p, g[t]);
+          p += gelems;
+        }
+      }
     }
   }
 }
@@ -165,6 +248,26 @@ __device__ __forceinline__ void st_quad(const CombineArgs& a, double* base, int6
   }
 }
 
+// the four quadrants C11, C12, C21, C22 of one node at one element position from its seven
+// products: P:279-282 (StrassenNaiv) / P:308-311 (StrassenWinograd), left to right as displayed
+template <int VARIANT>
+__device__ __forceinline__ void comb4(double H1, double H2, double H3, double H4, double H5, double H6, double H7,
+                                      double (&c)[4]) {
+  if (VARIANT == SV_NAIV) {  // P:279-282, left to right
+    c[0] = dadd(dsub(dadd(H1, H4), H5), H7);
+    c[1] = dadd(H3, H5);
+    c[2] = dadd(H2, H4);
+    c[3] = dadd(dsub(dadd(H1, H3), H2), H6);
+  } else {
+    const double H8 = dadd(H1, H3);
+    const double H9 = dadd(H8, H4);
+    c[0] = dadd(H1, H2);
+    c[1] = dadd(H9, H6);
+    c[2] = dadd(dadd(H8, H5), H7);
+    c[3] = dadd(H9, H5);
+  }
+}
+
 template <int VARIANT, int V>
 __global__ void __launch_bounds__(256) strassen_combine_kernel(CombineArgs a, int tprs) {
   const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
@@ -182,26 +285,72 @@ __global__ void __launch_bounds__(256) strassen_combine_kernel(CombineArgs a, in
       double c11[V], c12[V], c21[V], c22[V];
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        const double H1 = h[0][e], H2 = h[1][e], H3 = h[2][e], H4 = h[3][e], H5 = h[4][e], H6 = h[5][e],
-                     H7 = h[6][e];
-        if (VARIANT == SV_NAIV) {  // P:279-282, left to right
-          c11[e] = dadd(dsub(dadd(H1, H4), H5), H7);
-          c12[e] = dadd(H3, H5);
-          c21[e] = dadd(H2, H4);
-          c22[e] = dadd(dsub(dadd(H1, H3), H2), H6);
-        } else {
-          const double H8 = dadd(H1, H3);
-          const double H9 = dadd(H8, H4);
-          c11[e] = dadd(H1, H2);
-          c12[e] = dadd(H9, H6);
-          c21[e] = dadd(dadd(H8, H5), H7);
-          c22[e] = dadd(H9, H5);
-        }
+        double q4[4];
+        comb4<VARIANT>(h[0][e], h[1][e], h[2][e], h[3][e], h[4][e], h[5][e], h[6][e], q4);
+        c11[e] = q4[0];
+        c12[e] = q4[1];
+        c21[e] = q4[2];
+        c22[e] = q4[3];
       }
       st_quad<V>(a, base, i, j, c11);
       st_quad<V>(a, base, i, j + a.h_cols, c12);
       st_quad<V>(a, base, i + a.h_rows, j, c21);
       st_quad<V>(a, base, i + a.h_rows, j + a.h_cols, c22);
+    }
+  }
+}
+
+// Two recursion levels in one pass (level l + 2 products -> level l node): per position, the 49
+// grandchild products of a node give its 7 children's 4 quadrant values (comb4 per child), and
+// those give the node's 16 sub-blocks (comb4 per child quadrant) -- the same operations and order
+// as two single-level passes (bitwise), without writing and re-reading level l + 1.
+// CombineArgs: H holds 49 cnt grandchild products of h_rows x h_cols (a quarter of the node).
+template <int VARIANT, int V>
+__global__ void __launch_bounds__(256) strassen_combine2_kernel(CombineArgs a, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
+  const int64_t units = a.cnt * a.h_rows;
+  const int64_t gelems = a.h_rows * a.h_cols;
+  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* h0 = a.H + (49 * q) * gelems + i * a.h_cols;
+    double* base = a.dst + q * a.dst_stride;
+    for (int64_t j = int64_t(lt) * V; j < a.h_cols; j += step) {
+      double cq[7][4][V];  // child c's quadrant (0 = 11, 1 = 12, 2 = 21, 3 = 22) at this position
+      const double* hp = h0 + j;
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        double h[7][V];
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+          ldv<V>(hp, h[t]);
+          hp += gelems;
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          double q4[4];
+          comb4<VARIANT>(h[0][e], h[1][e], h[2][e], h[3][e], h[4][e], h[5][e], h[6][e], q4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cq[c][k][e] = q4[k];
+        }
+      }
+      // node quadrant QK at child-quadrant k: comb4 over the children's quadrant-k values
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double o[4][V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          double q4[4];
+          comb4<VARIANT>(cq[0][k][e], cq[1][k][e], cq[2][k][e], cq[3][k][e], cq[4][k][e], cq[5][k][e], cq[6][k][e],
+                         q4);
+#pragma unroll
+          for (int QK = 0; QK < 4; ++QK) o[QK][e] = q4[QK];
+        }
+        const int64_t sr = (k >> 1) * a.h_rows, sc = (k & 1) * a.h_cols;  // sub-block inside a quadrant
+#pragma unroll
+        for (int QK = 0; QK < 4; ++QK)
+          st_quad<V>(a, base, i + sr + (QK >> 1) * 2 * a.h_rows, j + sc + (QK & 1) * 2 * a.h_cols, o[QK]);
+      }
     }
   }
 }
@@ -321,6 +470,27 @@ cudaError_t launch_form_level(int side, const FormArgs& fa, int v, int sms, cuda
   return side == 0 ? launch_form_side<VARIANT, 0>(fa, v, sms, st) : launch_form_side<VARIANT, 1>(fa, v, sms, st);
 }
 
+template <int VARIANT, int SIDE>
+cudaError_t launch_form2_side(const FormArgs& fa, int v, int sms, cudaStream_t st) {
+  if (v > 2) v = 2;  // 16 inputs x V live per thread: V = 4 would spill (V = 1: same time)
+  const int64_t units = fa.cnt * fa.h_rows;
+  const int tprs = tpr_shift(fa.h_cols, v);
+  if (v == 2) {
+    constexpr auto k = strassen_form2_kernel<VARIANT, SIDE, 2>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  } else {
+    constexpr auto k = strassen_form2_kernel<VARIANT, SIDE, 1>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
+cudaError_t launch_form2_level(int side, const FormArgs& fa, int v, int sms, cudaStream_t st) {
+  return side == 0 ? launch_form2_side<VARIANT, 0>(fa, v, sms, st) : launch_form2_side<VARIANT, 1>(fa, v, sms, st);
+}
+
 template <int VARIANT>
 cudaError_t launch_combine_level(const CombineArgs& ca, int v, int sms, cudaStream_t st) {
   const int64_t units = ca.cnt * ca.h_rows;
@@ -340,6 +510,22 @@ cudaError_t launch_combine_level(const CombineArgs& ca, int v, int sms, cudaStre
 }
 
 template <int VARIANT>
+cudaError_t launch_combine2_level(const CombineArgs& ca, int v, int sms, cudaStream_t st) {
+  if (v > 2) v = 2;  // 28 child-quadrant values x V live per thread
+  const int64_t units = ca.cnt * ca.h_rows;
+  const int tprs = tpr_shift(ca.h_cols, v);
+  if (v == 2) {
+    constexpr auto k = strassen_combine2_kernel<VARIANT, 2>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(ca, tprs);
+  } else {
+    constexpr auto k = strassen_combine2_kernel<VARIANT, 1>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(ca, tprs);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
 cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
                          const StrassenPlan& pl, char* ws, int sms, cudaStream_t st) {
   const int d = pl.depth;
@@ -352,12 +538,25 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   double* T[2] = {reinterpret_cast<double*>(ws + pl.offT[0]), reinterpret_cast<double*>(ws + pl.offT[1])};
   double* Hb = reinterpret_cast<double*>(ws + pl.offH);
   double* Cb[2] = {reinterpret_cast<double*>(ws + pl.offC[0]), reinterpret_cast<double*>(ws + pl.offC[1])};
-  // level l >= 1 of S/T lives in buffer (d - l) % 2 ; combination level l >= 1 in Cb[(d - 1 - l) % 2]
+  // Formation schedule: single levels until the remaining depth is even, then two levels per
+  // pass (strassen_form2_kernel), so the deepest -- largest -- intermediate levels are never
+  // written.  The produced levels alternate between the two buffers, the last (level d, read
+  // by the leaf GEMM) in buffer 0; buffer 1 is sized for level d - 1 >= any earlier level.
+  // Combination level l >= 1 lives in Cb[(d - 1 - l) % 2].
+  int steps[16][2], ns = 0;
+  for (int l = 0; l < d;) {
+    const int to = ((d - l) % 2 == 0) ? l + 2 : l + 1;
+    steps[ns][0] = l;
+    steps[ns][1] = to;
+    ++ns;
+    l = to;
+  }
   for (int side = 0; side < 2; ++side) {
     NvtxRange nvtx(side == 0 ? "strassen form (A side)" : "strassen form (B side)");
     const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
     double** buf = side == 0 ? S : T;
-    for (int l = 0; l < d; ++l) {
+    for (int k = 0; k < ns; ++k) {
+      const int l = steps[k][0], two = steps[k][1] - l == 2;
       FormArgs fa;
       const int64_t r_l = R >> l, c_l = Ccols >> l;
       if (l == 0) {
@@ -367,18 +566,18 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
         fa.rows_valid = side == 0 ? N : P;
         fa.cols_valid = side == 0 ? P : M;
       } else {
-        fa.src = buf[(d - l) % 2];
+        fa.src = buf[(ns - k) % 2];  // level l was produced by step k - 1: buffer (ns - 1 - (k - 1)) % 2
         fa.src_pitch = c_l;
         fa.src_stride = r_l * c_l;
         fa.rows_valid = r_l;
         fa.cols_valid = c_l;
       }
-      fa.dst = buf[(d - l - 1) % 2];
-      fa.h_rows = r_l / 2;
-      fa.h_cols = c_l / 2;
+      fa.dst = buf[(ns - 1 - k) % 2];
+      fa.h_rows = two ? r_l / 4 : r_l / 2;
+      fa.h_cols = two ? c_l / 4 : c_l / 2;
       fa.cnt = ipow7(l);
       const int v = pick_vec(fa.src, fa.dst, fa.src_pitch, fa.src_stride, fa.h_cols);
-      e = launch_form_level<VARIANT>(side, fa, v, sms, st);
+      e = two ? launch_form2_level<VARIANT>(side, fa, v, sms, st) : launch_form_level<VARIANT>(side, fa, v, sms, st);
       if (e != cudaSuccess) return e;
     }
   }
@@ -391,10 +590,17 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
     if (e != cudaSuccess) return e;
   }
   NvtxRange nvtx_combine("strassen combination");
-  for (int l = d - 1; l >= 0; --l) {
+  // Combination schedule: two levels per pass from the deepest (largest) level down, a single
+  // level last when one remains; the k-th produced intermediate level lives in Cb[k % 2]
+  // (Cb[0] is sized for level d - 1, Cb[1] for d - 2 >= every later one).
+  const double* Hsrc = Hb;
+  int produced = 0;
+  for (int l_from = d; l_from > 0;) {
+    const int l = l_from >= 2 ? l_from - 2 : l_from - 1;  // the level this pass writes
+    const bool two = l_from - l == 2;
     CombineArgs ca;
     const int64_t r_l = pl.Np >> l, c_l = pl.Mp >> l;
-    ca.H = (l == d - 1) ? Hb : Cb[(d - 1 - (l + 1)) % 2];
+    ca.H = Hsrc;
     if (l == 0) {
       ca.dst = C;
       ca.dst_pitch = M;
@@ -402,18 +608,20 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
       ca.rows_valid = N;
       ca.cols_valid = M;
     } else {
-      ca.dst = Cb[(d - 1 - l) % 2];
+      ca.dst = Cb[produced % 2];
       ca.dst_pitch = c_l;
       ca.dst_stride = r_l * c_l;
       ca.rows_valid = r_l;
       ca.cols_valid = c_l;
     }
-    ca.h_rows = r_l / 2;
-    ca.h_cols = c_l / 2;
+    ca.h_rows = two ? r_l / 4 : r_l / 2;
+    ca.h_cols = two ? c_l / 4 : c_l / 2;
     ca.cnt = ipow7(l);
     const int v = pick_vec(ca.dst, ca.H, ca.dst_pitch, ca.dst_stride, ca.h_cols);
-    e = launch_combine_level<VARIANT>(ca, v, sms, st);
+    e = two ? launch_combine2_level<VARIANT>(ca, v, sms, st) : launch_combine_level<VARIANT>(ca, v, sms, st);
     if (e != cudaSuccess) return e;
+    if (l > 0) Hsrc = ca.dst, ++produced;
+    l_from = l;
   }
   return cudaSuccess;
 }
