@@ -16,7 +16,8 @@
 // All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
 //  * two levels per pass (strassen_form2_kernel / strassen_combine2_kernel) for the deepest
 //    pairs of levels: the intermediate level -- 7/4 the data of the one above it -- is never
-//    written nor re-read (c4, d = 3: 24.6 -> 23.0 ms per product).
+//    written nor re-read, and a three-level formation pass (strassen_form3_kernel) at odd depth
+//    (c4, d = 3: 24.6 -> 22.4 ms per product).
 #pragma once
 #include "common.cuh"
 #include "gemm_tma.cuh"
@@ -222,6 +223,61 @@ __global__ void __launch_bounds__(256) strassen_form2_kernel(FormArgs a, int tpr
         for (int t = 0; t < 7; ++t) {
           stv<V>(p, g[t]);
           p += gelems;
+        }
+      }
+    }
+  }
+}
+
+// Three recursion levels in one pass (l -> l + 3, scalar): a thread reads a node's 64 sub-block
+// values (8 x 8 grid) at one position; for each child c its 16 sub-block values, for each
+// grandchild g its 4 quadrant values, then the 7 great-grandchildren -- again exactly the
+// single-level operations in their order.  h_rows / h_cols: the great-grandchild dims (an
+// eighth of the parent's); dst holds 343 cnt nodes.  At d = 3 this is the whole formation.
+template <int VARIANT, int SIDE>
+__global__ void __launch_bounds__(256) strassen_form3_kernel(FormArgs a, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(1) << tprs;
+  const int64_t units = a.cnt * a.h_rows;
+  const int64_t gelems = a.h_rows * a.h_cols;
+  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* base = a.src + q * a.src_stride;
+    double* d0 = a.dst + (343 * q) * gelems + i * a.h_cols;
+    for (int64_t j = lt; j < a.h_cols; j += step) {
+      double x[8][8];
+#pragma unroll
+      for (int pr = 0; pr < 8; ++pr)
+#pragma unroll
+        for (int pc = 0; pc < 8; ++pc) {
+          double v[1];
+          ld_quad<1>(a, base, i + pr * a.h_rows, j + pc * a.h_cols, v);
+          x[pr][pc] = v[0];
+        }
+      double* p = d0 + j;
+#pragma unroll 1
+      for (int c = 0; c < 7; ++c) {
+        double ch[4][4];  // child c's 4 x 4 sub-blocks: child c of the parent quadrants' sub-blocks
+#pragma unroll
+        for (int ra = 0; ra < 4; ++ra)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb)
+            ch[ra][cb] = form1<VARIANT, SIDE>(c, x[ra][cb], x[ra][4 + cb], x[4 + ra][cb], x[4 + ra][4 + cb]);
+#pragma unroll 1
+        for (int g = 0; g < 7; ++g) {
+          double gq[2][2];
+#pragma unroll
+          for (int ra = 0; ra < 2; ++ra)
+#pragma unroll
+            for (int cb = 0; cb < 2; ++cb)
+              gq[ra][cb] = form1<VARIANT, SIDE>(g, ch[ra][cb], ch[ra][2 + cb], ch[2 + ra][cb], ch[2 + ra][2 + cb]);
+          double o[7];
+          form7<VARIANT, SIDE>(gq[0][0], gq[0][1], gq[1][0], gq[1][1], o);
+#pragma unroll
+          for (int t = 0; t < 7; ++t) {
+            *p = o[t];
+            p += gelems;
+          }
         }
       }
     }
@@ -486,6 +542,21 @@ cudaError_t launch_form2_side(const FormArgs& fa, int v, int sms, cudaStream_t s
   return cudaGetLastError();
 }
 
+template <int VARIANT, int SIDE>
+cudaError_t launch_form3_side(const FormArgs& fa, int sms, cudaStream_t st) {
+  const int64_t units = fa.cnt * fa.h_rows;
+  const int tprs = tpr_shift(fa.h_cols, 1);
+  constexpr auto k = strassen_form3_kernel<VARIANT, SIDE>;
+  k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
+cudaError_t launch_form3_level(int side, const FormArgs& fa, int sms, cudaStream_t st) {
+  return side == 0 ? launch_form3_side<VARIANT, 0>(fa, sms, st) : launch_form3_side<VARIANT, 1>(fa, sms, st);
+}
+
 template <int VARIANT>
 cudaError_t launch_form2_level(int side, const FormArgs& fa, int v, int sms, cudaStream_t st) {
   return side == 0 ? launch_form2_side<VARIANT, 0>(fa, v, sms, st) : launch_form2_side<VARIANT, 1>(fa, v, sms, st);
@@ -538,14 +609,15 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   double* T[2] = {reinterpret_cast<double*>(ws + pl.offT[0]), reinterpret_cast<double*>(ws + pl.offT[1])};
   double* Hb = reinterpret_cast<double*>(ws + pl.offH);
   double* Cb[2] = {reinterpret_cast<double*>(ws + pl.offC[0]), reinterpret_cast<double*>(ws + pl.offC[1])};
-  // Formation schedule: single levels until the remaining depth is even, then two levels per
-  // pass (strassen_form2_kernel), so the deepest -- largest -- intermediate levels are never
-  // written.  The produced levels alternate between the two buffers, the last (level d, read
+  // Formation schedule: an odd remaining depth >= 3 starts with a three-level pass
+  // (strassen_form3_kernel), then two levels per pass (strassen_form2_kernel), a single level
+  // only when d = 1, so the deepest -- largest -- intermediate levels are never written.  The produced levels alternate between the two buffers, the last (level d, read
   // by the leaf GEMM) in buffer 0; buffer 1 is sized for level d - 1 >= any earlier level.
   // Combination level l >= 1 lives in Cb[(d - 1 - l) % 2].
   int steps[16][2], ns = 0;
   for (int l = 0; l < d;) {
-    const int to = ((d - l) % 2 == 0) ? l + 2 : l + 1;
+    const int r = d - l;  // remaining levels: an odd remainder >= 3 starts with a triple pass
+    const int to = (r % 2 == 1 && r >= 3) ? l + 3 : (r >= 2 ? l + 2 : l + 1);
     steps[ns][0] = l;
     steps[ns][1] = to;
     ++ns;
@@ -556,7 +628,7 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
     const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
     double** buf = side == 0 ? S : T;
     for (int k = 0; k < ns; ++k) {
-      const int l = steps[k][0], two = steps[k][1] - l == 2;
+      const int l = steps[k][0], span = steps[k][1] - l, two = span == 2;
       FormArgs fa;
       const int64_t r_l = R >> l, c_l = Ccols >> l;
       if (l == 0) {
@@ -573,11 +645,13 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
         fa.cols_valid = c_l;
       }
       fa.dst = buf[(ns - 1 - k) % 2];
-      fa.h_rows = two ? r_l / 4 : r_l / 2;
-      fa.h_cols = two ? c_l / 4 : c_l / 2;
+      fa.h_rows = r_l >> span;
+      fa.h_cols = c_l >> span;
       fa.cnt = ipow7(l);
       const int v = pick_vec(fa.src, fa.dst, fa.src_pitch, fa.src_stride, fa.h_cols);
-      e = two ? launch_form2_level<VARIANT>(side, fa, v, sms, st) : launch_form_level<VARIANT>(side, fa, v, sms, st);
+      e = span == 3 ? launch_form3_level<VARIANT>(side, fa, sms, st)
+          : two     ? launch_form2_level<VARIANT>(side, fa, v, sms, st)
+                    : launch_form_level<VARIANT>(side, fa, v, sms, st);
       if (e != cudaSuccess) return e;
     }
   }
