@@ -25,6 +25,7 @@ def family(name: str) -> str:
         return "line_kernel<1> (winograd y/z)"
     for k in ("dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_tma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
               "winograd_kernel",
+              "strassen_form3_kernel", "strassen_form2_kernel", "strassen_combine2_kernel",
               "strassen_form_kernel", "strassen_combine_kernel", "norm_inf_kernel", "scale_copy_kernel",
               "lambda_kernel"):
         if k in name:
