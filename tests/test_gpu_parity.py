@@ -308,26 +308,37 @@ def test_c4_sampled(method, levels, c4_ops):
 
 
 # ------------------------------------------------------------------ config c5: one rank's shard of the 8-GPU run
-def test_c5_rank_shard_sampled():
-    """BASELINE.json config 5 (32768^3) as one rank of the 8-GPU row-block run sees it:
-    rows [0, 4096) of A times the full B.  2048 seeded entries per method, bitwise against
-    the oracle (classical and Strassen-Winograd, the two methods config 5 names)."""
+@pytest.fixture(scope="module")
+def c5_B():
+    return workload.matrix(workload.CONFIGS["c5"], 1, 0)
+
+
+@pytest.mark.parametrize("world,rank", [(8, 0), (8, 7), (2, 1)])
+def test_c5_rank_shard_sampled(world, rank, c5_B):
+    """BASELINE.json config 5 (32768^3) as one rank of the g-GPU row-block run sees it:
+    its rows of A (regenerated independently, workload's 1024-row chunks) times the full B.
+    2048 seeded entries per shard and method, bitwise against the oracle (classical and
+    Strassen-Winograd, the two methods config 5 names); g = 2 gives a 16384-row shard."""
     cfg = workload.CONFIGS["c5"]
-    lo, hi = workload.shard_rows(cfg.N, 8, 0)
+    lo, hi = workload.shard_rows(cfg.N, world, rank)
     A = workload.matrix(cfg, 0, 0, lo, hi)
-    B = workload.matrix(cfg, 1, 0)
+    B = c5_B
     dA, dB = dev(A), dev(B)
     N, P, M = A.shape[0], A.shape[1], B.shape[1]
-    idx = _sample(5, N, M, 2048, shard=0)
-    C = host(mm.naive(dA, dB))
+    idx = _sample(5, N, M, 2048, shard=rank)
+    ii = torch.tensor([i for i, _ in idx], device=DEV)
+    jj = torch.tensor([j for _, j in idx], device=DEV)
+    C = mm.naive(dA, dB)
     ref = oracle.entries(oracle.M_FMA, A, B, idx)
-    assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
+    assert np.array_equal(C[ii, jj].cpu().numpy(), ref)
     del C
-    C = host(mm.strassen_winograd(dA, dB, levels=2))
+    C = mm.strassen_winograd(dA, dB, levels=2)
     d, pad = plan_pad(N, P, M, 2)
     ref = oracle.entries_strassen(1, A, B, idx, levels=d, pad=pad, base=oracle.BASE_FMA)
-    assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
+    assert np.array_equal(C[ii, jj].cpu().numpy(), ref)
+    del C, dA, dB
     mm.release_workspace()
+    torch.cuda.empty_cache()
 
 
 def test_host_matmul_pipelined_bitwise():
