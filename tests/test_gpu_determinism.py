@@ -41,3 +41,36 @@ def test_panel_accumulation_stress(ops):
         for i, (k0, k1) in enumerate(panel_bounds(8192, panels)):
             mm.naive_panel(A[:, k0:k1], B[k0:k1], C, accumulate=i > 0)
         assert torch.equal(C, ref), panels
+
+
+@pytest.mark.parametrize("method", ["strassen", "strassen_winograd"])
+def test_repeatable_bits_strassen_depth3(ops, method):
+    """bench.py's Strassen depth: the three-level formation pass and the two-level combination."""
+    A, B = ops
+    f = getattr(mm, method)
+    ref = f(A, B, levels=3)
+    out = torch.empty_like(ref)
+    for _ in range(3):
+        f(A, B, out=out, levels=3)
+        assert torch.equal(out, ref), method
+
+
+def test_kahan_winograd_panel_stress(ops):
+    """The state-carrying K2 / K3 panel steps (NEXT-4) at full size, repeated."""
+    from paper_1106_1347_b200.dist import panel_bounds
+
+    A, B = ops
+    C = torch.empty(8192, 8192, dtype=torch.float64, device="cuda")
+    E = torch.empty_like(C)
+    y = torch.empty(8192, dtype=torch.float64, device="cuda")
+    z = torch.empty(8192, dtype=torch.float64, device="cuda")
+    ref_k, ref_w = mm.kahan(A, B), mm.winograd(A, B)
+    mm.winograd_yz(A, B, y, z)
+    for panels in (3, 4):
+        b = panel_bounds(8192, panels)
+        for i, (k0, k1) in enumerate(b):
+            mm.kahan_panel(A[:, k0:k1], B[k0:k1], C, E, accumulate=i > 0, keep_state=k1 < 8192)
+        assert torch.equal(C, ref_k), ("kahan", panels)
+        for i, (k0, k1) in enumerate(b):
+            mm.winograd_panel(A[:, k0:k1], B[k0:k1], C, y, z, accumulate=i > 0, keep_state=k1 < 8192)
+        assert torch.equal(C, ref_w), ("winograd", panels)
