@@ -53,9 +53,11 @@ struct GemmCfg {
 // (tools/tune/gemm_tune.cu compares the alternatives; profiles/r01/gemm_tune*.jsonl).
 // Two independent CTAs per SM let one CTA's barrier/refill overlap the other's DMMAs.
 using GemmDefault = GemmCfg<128, 64, 2, 2, 4, 2>;
-// small problems (fewer than two full waves of default tiles): 64 x 64 tiles, 4 warps of 32 x 32,
-// 4 CTAs per SM -- 4x the tiles, so e.g. 2048^3 fills the 148 SMs (31.2 vs 29.5 TF measured)
-using GemmSmall = GemmCfg<64, 64, 2, 2, 4, 4>;
+// small problems (fewer than two full waves of default tiles) and every odd-pitch A: 64 x 64
+// tiles, 4 warps of 32 x 32, 3 stages, 3 CTAs per SM (4 CTAs per SM cap the registers at 128:
+// c3 4096 x 1001 x 3000 0.795 vs 0.848 ms, 8192 x 8191 x 8192 33.4 vs 35.5 ms, 2048 x 2047 x 2048
+// 0.550 vs 0.587 ms; tools/tune/gemm_tune.cu c3, profiles/r01/gemm_tune_oddP.jsonl)
+using GemmSmall = GemmCfg<64, 64, 2, 2, 3, 3>;
 
 template <class CF, int AV, int BV>
 __device__ __forceinline__ void gemm_load_tile(double* As, double* Bs, const double* __restrict__ A,
@@ -246,8 +248,8 @@ inline cudaError_t launch_dgemm_cfg(const GemmProblem& pr, cudaStream_t st) {
 
 // tile configuration by problem size (the per-entry arithmetic is identical for both)
 // Operands reaching this path are those TMA cannot describe; when A's rows are only 8-byte
-// aligned (odd P) the 64 x 64 / 4-CTA configuration is faster at every size measured (c3
-// 4096 x 1001 x 3000: 0.85 vs 1.06 ms; 8192 x 8191 x 8192: 30.9 vs 27.9 TF;
+// aligned (odd P) the 64 x 64 configuration is faster than 128 x 64 at every size measured (c3
+// 4096 x 1001 x 3000: 0.85 vs 1.06 ms at 4 CTAs per SM, 0.795 ms at 3; 8192 x 8191 x 8192: 30.9 vs 27.9 TF;
 // profiles/r01/gemm_tune_oddP.jsonl)
 // tiny batched problems with an odd pitch (the paper plan's order-17 leaves): one warp per
 // 32 x 32 tile

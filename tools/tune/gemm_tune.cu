@@ -93,6 +93,12 @@ int main(int argc, char** argv) {
     fill<<<1024, 256>>>(B, 1002 * 3000, 2);
     run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 2, 3, 32>, false>("cpasync_64x64_s2_3cta_bk32_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 2, 32>, false>("cpasync_64x64_s3_2cta_bk32_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 3, 16>, false>("cpasync_64x64_s3_3cta_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 5, 3, 16>, false>("cpasync_64x64_s5_3cta_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 3, 16>, false>("cpasync_64x64_s4_3cta_P1001", A, B, C, 4096, 1001, 3000, 20);
+    run_rect<GemmCfg<64, 64, 2, 2, 2, 3, 16>, false>("cpasync_64x64_s2_3cta_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<64, 32, 2, 1, 4, 6>, false>("cpasync_64x32_w2x1_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<32, 64, 1, 2, 4, 6>, false>("cpasync_32x64_w1x2_P1001", A, B, C, 4096, 1001, 3000, 20);
     run_rect<GemmCfg<64, 64, 2, 2, 3, 4>, false>("cpasync_64x64_s3_P1001", A, B, C, 4096, 1001, 3000, 20);
@@ -108,6 +114,12 @@ int main(int argc, char** argv) {
     fill<<<1024, 256>>>(B2, 8192ll * 8192, 2);
     run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 2, 3, 32>, false>("cpasync_64x64_s2_3cta_bk32_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 2, 32>, false>("cpasync_64x64_s3_2cta_bk32_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 3, 16>, false>("cpasync_64x64_s3_3cta_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 3, 16>, false>("cpasync_64x64_s4_3cta_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
+    run_rect<GemmCfg<64, 64, 2, 2, 3, 3, 16>, false>("cpasync_64x64_s3_3cta_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
+    run_rect<GemmCfg<64, 64, 2, 2, 4, 3, 16>, false>("cpasync_64x64_s4_3cta_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
     run_rect<GemmCfg<64, 64, 2, 2, 3, 4>, false>("cpasync_64x64_s3_P8191", A2, B2, C2, 8192, 8191, 8192, 3);
     run_rect<GemmCfg<128, 64, 2, 2, 4, 2>, false>("cpasync_128x64_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
     run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);

@@ -126,9 +126,15 @@ int main(int argc, char** argv) {
     rect<SimtCfg<128, 64, 8, 8, 3, 2>>("winograd", "128x64_t8x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
     rect<SimtCfg<64, 64, 4, 8, 3, 2>>("winograd", "64x64_t4x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
     rect<SimtCfg<64, 64, 8, 8, 3, 4>>("winograd", "64x64_t8x8_s3_4cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<96, 64, 6, 8, 3, 3>>("winograd", "96x64_t6x8_s3_3cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<96, 64, 6, 8, 2, 3>>("winograd", "96x64_t6x8_s2_3cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<128, 64, 8, 8, 2, 2>>("winograd", "128x64_t8x8_s2_2cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<128, 64, 8, 8, 3, 2, 32>>("winograd", "128x64_t8x8_s3_2cta_bk32", A, B, C, y, z, 4096, 1001, 3000);
     rect<SimtCfg<64, 64, 4, 8, 3, 2>>("kahan", "64x64_t4x8_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
     rect<SimtCfg<64, 64, 8, 4, 3, 2>>("kahan", "64x64_t8x4_s3_2cta", A, B, C, y, z, 4096, 1001, 3000);
     rect<SimtCfg<32, 64, 4, 8, 3, 3>>("kahan", "32x64_t4x8_s3_3cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<48, 64, 3, 8, 3, 3>>("kahan", "48x64_t3x8_s3_3cta", A, B, C, y, z, 4096, 1001, 3000);
+    rect<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("kahan", "64x64_t4x8_s2_2cta_bk32", A, B, C, y, z, 4096, 1001, 3000);
     return 0;
   }
   const bool wino_only = argc > 1 && argv[1][0] == 'w';
