@@ -152,6 +152,28 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
   fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
   // SimtCfg<BM, BN, TM, TN, STAGES, MINB, BK>
+  if (argc > 1 && argv[1][0] == 's') {  // 1024^3 (config c2): small-grid configurations, cp.async kernels
+    c.n = 1024;
+    c.reps = 20;
+    cudaMalloc(&c.A, c.n * c.n * 8);
+    cudaMalloc(&c.B, c.n * c.n * 8);
+    cudaMalloc(&c.C, c.n * c.n * 8);
+    cudaMalloc(&c.R, c.n * c.n * 8);
+    cudaMalloc(&c.y, c.n * 8);
+    cudaMalloc(&c.z, c.n * 8);
+    cudaMalloc(&c.bad, 8);
+    fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
+    fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
+    wino<SimtCfg<64, 64, 4, 8, 3, 2>>("wino_64x64_t4x8_s3_2cta", c, true);
+    wino<SimtCfg<32, 32, 2, 4, 3, 4>>("wino_32x32_t2x4_s3_4cta", c, false);
+    wino<SimtCfg<64, 32, 4, 4, 3, 4>>("wino_64x32_t4x4_s3_4cta", c, false);
+    wino<SimtCfg<32, 64, 2, 8, 3, 4>>("wino_32x64_t2x8_s3_4cta", c, false);
+    wino<SimtCfg<64, 64, 8, 8, 3, 4>>("wino_64x64_t8x8_s3_4cta", c, false);
+    kahan<SimtCfg<32, 32, 2, 4, 3, 4>>("kahan_32x32_t2x4_s3_4cta", c, true);
+    kahan<SimtCfg<32, 32, 2, 4, 4, 6>>("kahan_32x32_t2x4_s4_6cta", c, false);
+    kahan<SimtCfg<32, 64, 2, 8, 3, 4>>("kahan_32x64_t2x8_s3_4cta", c, false);
+    return 0;
+  }
   if (kahan_only) {  // K2 configurations only
     kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
     kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_2cta_bk32", c);
