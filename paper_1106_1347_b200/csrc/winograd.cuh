@@ -32,6 +32,8 @@ namespace mmk {
 // big tiles would leave SMs idle (tools/tune/simt_tune.cu, profiles/r01/simt_tune*.jsonl)
 using WinogradDefault = SimtCfg<128, 64, 8, 8, 3, 2>;
 using WinogradSmall = SimtCfg<64, 64, 4, 8, 3, 2>;
+// cp.async alternative with a finer tile grid (better last-wave fill on some shapes)
+using Winograd96 = SimtCfg<96, 64, 6, 8, 2, 3>;
 // TMA-fed main loop (simt_tma.cuh) for 16-byte aligned operands with P, M even: 32-deep k tiles,
 // double-buffered -- 65.1 vs 65.6 ms (16-deep, 4 stages) at 8192^3
 using WinogradTma = SimtCfg<128, 64, 8, 8, 2, 2, 32>;
@@ -171,6 +173,13 @@ inline cudaError_t launch_winograd_pairs(const double* A, const double* B, doubl
   if (big_tiles >= 2 * int64_t(sms)) {
     if (simt_tma_ok(A, B, N, P, M))
       return launch_winograd_pairs_tma<WinogradTma, FUSED>(A, B, C, y, z, N, P, M, st);
+    // cp.async path: 128 x 64 tiles at 2 CTAs/SM unless 96 x 64 tiles at 3 CTAs/SM (3% slower per
+    // tile) fill their last wave enough better -- e.g. c3, 5.08 vs 4.55 waves: 1.73 vs 1.78 ms
+    // (profiles/r01/simt_tune_c3_v2.jsonl)
+    const int64_t t96 = cdiv(N, Winograd96::BM) * cdiv(M, Winograd96::BN);
+    const double f128 = double(big_tiles) / double(cdiv(big_tiles, 2 * int64_t(sms)) * 2 * sms);
+    const double f96 = 0.97 * double(t96) / double(cdiv(t96, 3 * int64_t(sms)) * 3 * sms);
+    if (f96 > f128) return launch_winograd_main<Winograd96, FUSED>(A, B, C, y, z, N, P, M, st);
     return launch_winograd_main<WinogradDefault, FUSED>(A, B, C, y, z, N, P, M, st);
   }
   return launch_winograd_main<WinogradSmall, FUSED>(A, B, C, y, z, N, P, M, st);
