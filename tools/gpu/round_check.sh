@@ -9,6 +9,13 @@ tail -3 gpurun_out/pytest_gpu.txt
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 cat gpurun_out/bench.json
 [ "${NO_NCU:-0}" = 1 ] || timeout 1200 bash tools/ncu_round.sh
+# summarise the ncu round here and drop two of the three --set full reports (gpurun copies back
+# at most 64 MiB of gpurun_out/; the Kahan report is kept for source-level reading)
+mkdir -p gpurun_out/ncu_sum
+python tools/ncu_summary.py gpurun_out/ncu gpurun_out/ncu_sum > /dev/null 2>&1
+python tools/hbm_table.py gpurun_out/ncu/hbm_kernels.csv > gpurun_out/ncu_sum/hbm_kernels.md 2>/dev/null
+python tools/fingerprint.py summarize gpurun_out/ncu/fingerprint.csv > gpurun_out/ncu_sum/fingerprint.md 2>/dev/null
+rm -f gpurun_out/ncu/full_naive.ncu-rep gpurun_out/ncu/full_winograd.ncu-rep
 # the paper's section-3 experiment on the GPU (Python and plain-C clients) and the per-config table
 timeout 900 python tools/paper_experiment.py --sizes 200,400,800,1600,3200,4096,8192 --json gpurun_out/paper_experiment.jsonl > gpurun_out/paper_experiment.txt 2>&1; echo paper rc=$?
 ./tools/mmtest -O 800 -R 10 > gpurun_out/mmtest.txt 2>&1; echo mmtest rc=$?

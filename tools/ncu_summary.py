@@ -142,8 +142,9 @@ def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "pr
            "```", json.dumps(traffic, indent=1), "```"]
     with open(os.path.join(dst, "ncu_summary.md"), "w") as f:
         f.write("\n".join(md) + "\n")
-    with open(os.path.join(ROOT, "profiles", "kernel_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    for d in {os.path.join(ROOT, "profiles"), dst}:
+        with open(os.path.join(d, "kernel_traffic.json"), "w") as f:
+            json.dump(traffic, f, indent=1)
     # the raw ncu launch list and HBM-kernel metrics (small CSVs) travel with the summary
     for name in ("launches.csv", "hbm_kernels.csv"):
         if os.path.exists(os.path.join(src, name)):
