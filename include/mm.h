@@ -112,7 +112,8 @@ int mm_kahan_ex(const double* A, int64_t lda, const double* B, int64_t ldb, doub
 int mm_winograd_ex(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, const double* y,
                    const double* z, int64_t N, int64_t K, int64_t M, int32_t flags, void* stream);
 /* y_i and z_k of P:189 (sums in increasing j; fma when flags & MM_EX_FUSED) of dense A (N x P) and
- * B (P x M) into device vectors y (N) and z (M). */
+ * B (P x M) into device vectors y (N) and z (M).  MM_ERR_ALIAS if y or z overlaps A, B or each
+ * other (mm_winograd_ex likewise if C overlaps y or z). */
 int mm_winograd_yz(const double* A, const double* B, int64_t N, int64_t P, int64_t M, double* y, double* z,
                    int32_t flags, void* stream);
 

@@ -180,6 +180,7 @@ int mm_winograd_ex(const double* A, int64_t lda, const double* B, int64_t ldb, d
   if (rc) return rc;
   if (K % 2 != 0) return MM_ERR_ARG;  // whole pairs per panel
   if (!(flags & MM_EX_KEEP_STATE) && (!y || !z)) return MM_ERR_ARG;
+  if ((y && overlaps(C, N * M, y, N)) || (z && overlaps(C, N * M, z, M))) return MM_ERR_ALIAS;
   if ((rc = check_device(nullptr))) return rc;
   const int f = ex_flags(flags);
   return cuda_status(
@@ -193,6 +194,9 @@ int mm_winograd_yz(const double* A, const double* B, int64_t N, int64_t P, int64
   mmk::NvtxRange nvtx("mm_winograd_yz");
   if (!A || !B || !y || !z || N < 1 || P < 1 || M < 1 || !mul_ok(N, P) || !mul_ok(P, M)) return MM_ERR_ARG;
   if (flags & ~MM_EX_FUSED) return MM_ERR_ARG;
+  if (overlaps(y, N, A, N * P) || overlaps(y, N, B, P * M) || overlaps(z, M, A, N * P) ||
+      overlaps(z, M, B, P * M) || overlaps(y, N, z, M))
+    return MM_ERR_ALIAS;
   int rc = check_device(nullptr);
   if (rc) return rc;
   return cuda_status(mmk::launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, S(stream),

@@ -109,6 +109,12 @@ def test_panel_ex_argument_errors():
     assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 9, 6, 2, None) == -1  # odd panel width
     assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), None, None, 8, 10, 6, 0, None) == -1  # epilogue needs y, z
     assert L.mm_kahan_ex(p(A), 10, p(B), 6, p(C), p(E), 8, 10, 6, 2, None) == 0
+    y = torch.zeros(8, dtype=torch.float64, device=DEV)
+    z = torch.zeros(6, dtype=torch.float64, device=DEV)
+    assert L.mm_winograd_yz(p(A), p(B), 8, 10, 6, p(A), p(z), 0, None) == -2   # y aliases A
+    assert L.mm_winograd_yz(p(A), p(B), 8, 10, 6, p(y), p(y), 0, None) == -2   # z aliases y
+    assert L.mm_winograd_ex(p(A), 10, p(B), 6, p(C), p(C), p(z), 8, 10, 6, 0, None) == -2  # y inside C
+    assert L.mm_winograd_yz(p(A), p(B), 8, 10, 6, p(y), p(z), 0, None) == 0
 
 
 def test_random_panel_splits_all_row_local_methods():
