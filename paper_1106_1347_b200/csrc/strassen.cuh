@@ -4,20 +4,20 @@
 //  level l holds 7^l nodes; node q's operands are dense [n_l x p_l] / [p_l x m_l] blocks at
 //  q * n_l * p_l of the level buffer; child t (t = 0..6 for H_{t+1}) of node q is node 7q + t.
 //
-//  * form kernel (one launch per level and side): reads the four quadrants X11, X12, X21,
+//  * form kernel (one launch per level and side, or per two / three levels, below): reads the four quadrants X11, X12, X21,
 //    X22 of every node once and writes the seven child operands, fusing the paper's block
 //    additions (P:271-277 / P:300-306) in registers with exactly the oracle's per-element
 //    operations and order (e.g. A2 = A22 - (A11 - A21)).  At level 0 it reads the caller's A
 //    or B with the zero embedding of P:286 applied on the fly (no padded copy).
-//  * the 7^d leaf products H = S T run as ONE batched DMMA GEMM launch (gemm_dmma.cuh).
+//  * the 7^d leaf products H = S T run as ONE batched DMMA GEMM launch (gemm_tma.cuh / gemm_dmma.cuh).
 //  * combine kernel (one launch per level): reads H_1..H_7 of every node once and writes
 //    the four C quadrants (P:279-282 / P:307-311, left to right as displayed); at level 0
 //    it writes straight into the caller's C, dropping the padding (the "extract" of P:286).
-// All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
 //  * two levels per pass (strassen_form2_kernel / strassen_combine2_kernel) for the deepest
 //    pairs of levels: the intermediate level -- 7/4 the data of the one above it -- is never
 //    written nor re-read, and a three-level formation pass (strassen_form3_kernel) at odd depth
 //    (c4, d = 3: 24.6 -> 22.4 ms per product).
+// All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
 #pragma once
 #include "common.cuh"
 #include "gemm_tma.cuh"
