@@ -4,12 +4,14 @@
 //  level l holds 7^l nodes; node q's operands are dense [n_l x p_l] / [p_l x m_l] blocks at
 //  q * n_l * p_l of the level buffer; child t (t = 0..6 for H_{t+1}) of node q is node 7q + t.
 //
-//  * form kernel (one launch per level and side, or per two / three levels, below): reads the four quadrants X11, X12, X21,
-//    X22 of every node once and writes the seven child operands, fusing the paper's block
+//  * form kernel (one launch per level and side, or per two / three levels, below): reads the
+//    four quadrants X11, X12, X21, X22 of every node once and writes the seven child operands,
+//    fusing the paper's block
 //    additions (P:271-277 / P:300-306) in registers with exactly the oracle's per-element
 //    operations and order (e.g. A2 = A22 - (A11 - A21)).  At level 0 it reads the caller's A
 //    or B with the zero embedding of P:286 applied on the fly (no padded copy).
-//  * the 7^d leaf products H = S T run as ONE batched DMMA GEMM launch (gemm_tma.cuh / gemm_dmma.cuh).
+//  * the 7^d leaf products H = S T run as ONE batched DMMA GEMM launch (gemm_tma.cuh, or
+//    gemm_dmma.cuh for operands a tensor map cannot describe).
 //  * combine kernel (one launch per level): reads H_1..H_7 of every node once and writes
 //    the four C quadrants (P:279-282 / P:307-311, left to right as displayed); at level 0
 //    it writes straight into the caller's C, dropping the padding (the "extract" of P:286).
