@@ -181,6 +181,8 @@ int main(int argc, char** argv) {
     kahan_tma<SimtCfg<64, 64, 4, 8, 4, 3, 16>>("tma_64x64_s4_3cta_bk16", c);
     kahan_tma<SimtCfg<48, 64, 3, 8, 4, 3, 16>>("tma_48x64_t3x8_s4_3cta_bk16", c);
     kahan_tma<SimtCfg<48, 64, 3, 8, 2, 3, 32>>("tma_48x64_t3x8_s2_3cta_bk32", c);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 6, 2, 16>>("tma_64x64_s6_2cta_bk16", c);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 5, 2, 16>>("tma_64x64_s5_2cta_bk16", c);
     return 0;
   }
   if (wino_only) {  // K3 configurations only
