@@ -429,6 +429,36 @@ inline int64_t ipow7(int d) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Formation schedule (levels from -> to per pass): an odd remaining depth >= 3 starts with a
+// three-level pass, then two levels per pass, a single level only when d = 1.  The produced
+// levels alternate between two buffers, the last (level d, read by the leaf GEMM) in buffer 0:
+// pass k writes buffer (ns - 1 - k) % 2.
+inline int form_schedule(int d, int (*steps)[2]) {
+  int ns = 0;
+  for (int l = 0; l < d;) {
+    const int r = d - l;
+    const int to = (r % 2 == 1 && r >= 3) ? l + 3 : (r >= 2 ? l + 2 : l + 1);
+    steps[ns][0] = l;
+    steps[ns][1] = to;
+    ++ns;
+    l = to;
+  }
+  return ns;
+}
+// Combination schedule: two levels per pass from the deepest level down, a single level last
+// when one remains; the k-th pass writing an intermediate level (> 0) uses buffer k % 2.
+inline int combine_schedule(int d, int (*steps)[2]) {
+  int ns = 0;
+  for (int l_from = d; l_from > 0;) {
+    const int l = l_from >= 2 ? l_from - 2 : l_from - 1;
+    steps[ns][0] = l_from;
+    steps[ns][1] = l;
+    ++ns;
+    l_from = l;
+  }
+  return ns;
+}
+
 // levels >= 0: pad each dim to a multiple of 2^(levels+1) (keeps every level's row pitch
 // even, so 16-byte vectors apply); levels == -1: the paper's square plan.
 inline bool make_strassen_plan(int64_t N, int64_t P, int64_t M, int levels, StrassenPlan* pl) {
@@ -457,11 +487,26 @@ inline bool make_strassen_plan(int64_t N, int64_t P, int64_t M, int levels, Stra
     if (l <= 0) return 0;
     return size_t(ipow7(l)) * size_t(r >> l) * size_t(c >> l) * sizeof(double);
   };
-  size_t off = 0;
-  const size_t s0 = lvl(d, pl->Np, pl->Pp), s1 = lvl(d - 1, pl->Np, pl->Pp);
-  const size_t t0 = lvl(d, pl->Pp, pl->Mp), t1 = lvl(d - 1, pl->Pp, pl->Mp);
+  // buffers sized for exactly the levels the schedules write into them
+  int fs[16][2], cs[16][2];
+  const int nf = form_schedule(d, fs), nc = combine_schedule(d, cs);
+  size_t s0 = 0, s1 = 0, t0 = 0, t1 = 0, c0 = 0, c1 = 0;
+  for (int k = 0; k < nf; ++k) {
+    const int l = fs[k][1];
+    size_t& sb = ((nf - 1 - k) % 2) ? s1 : s0;
+    size_t& tb = ((nf - 1 - k) % 2) ? t1 : t0;
+    sb = sb > lvl(l, pl->Np, pl->Pp) ? sb : lvl(l, pl->Np, pl->Pp);
+    tb = tb > lvl(l, pl->Pp, pl->Mp) ? tb : lvl(l, pl->Pp, pl->Mp);
+  }
+  for (int k = 0, produced = 0; k < nc; ++k) {
+    const int l = cs[k][1];
+    if (l == 0) continue;
+    size_t& cb = (produced % 2) ? c1 : c0;
+    cb = cb > lvl(l, pl->Np, pl->Mp) ? cb : lvl(l, pl->Np, pl->Mp);
+    ++produced;
+  }
   const size_t h = lvl(d, pl->Np, pl->Mp);
-  const size_t c0 = lvl(d - 1, pl->Np, pl->Mp), c1 = lvl(d - 2, pl->Np, pl->Mp);
+  size_t off = 0;
   pl->offS[0] = off; off = align256(off + s0);
   pl->offS[1] = off; off = align256(off + s1);
   pl->offT[0] = off; off = align256(off + t0);
@@ -616,15 +661,8 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   // only when d = 1, so the deepest -- largest -- intermediate levels are never written.  The produced levels alternate between the two buffers, the last (level d, read
   // by the leaf GEMM) in buffer 0; buffer 1 is sized for level d - 1 >= any earlier level.
   // Combination level l >= 1 lives in Cb[(d - 1 - l) % 2].
-  int steps[16][2], ns = 0;
-  for (int l = 0; l < d;) {
-    const int r = d - l;  // remaining levels: an odd remainder >= 3 starts with a triple pass
-    const int to = (r % 2 == 1 && r >= 3) ? l + 3 : (r >= 2 ? l + 2 : l + 1);
-    steps[ns][0] = l;
-    steps[ns][1] = to;
-    ++ns;
-    l = to;
-  }
+  int steps[16][2];
+  const int ns = form_schedule(d, steps);
   for (int side = 0; side < 2; ++side) {
     NvtxRange nvtx(side == 0 ? "strassen form (A side)" : "strassen form (B side)");
     const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
@@ -671,8 +709,10 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   // (Cb[0] is sized for level d - 1, Cb[1] for d - 2 >= every later one).
   const double* Hsrc = Hb;
   int produced = 0;
-  for (int l_from = d; l_from > 0;) {
-    const int l = l_from >= 2 ? l_from - 2 : l_from - 1;  // the level this pass writes
+  int csteps[16][2];
+  const int ncs = combine_schedule(d, csteps);
+  for (int k = 0; k < ncs; ++k) {
+    const int l_from = csteps[k][0], l = csteps[k][1];  // this pass reads level l_from, writes level l
     const bool two = l_from - l == 2;
     CombineArgs ca;
     const int64_t r_l = pl.Np >> l, c_l = pl.Mp >> l;
@@ -697,7 +737,6 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
     e = two ? launch_combine2_level<VARIANT>(ca, v, sms, st) : launch_combine_level<VARIANT>(ca, v, sms, st);
     if (e != cudaSuccess) return e;
     if (l > 0) Hsrc = ca.dst, ++produced;
-    l_from = l;
   }
   return cudaSuccess;
 }
