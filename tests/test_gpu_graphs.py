@@ -12,12 +12,13 @@ pytestmark = pytest.mark.gpu
 mm = pytest.importorskip("paper_1106_1347_b200")
 
 
-@pytest.mark.parametrize("method", ["naive", "kahan", "winograd", "winograd_scaled", "strassen", "strassen_winograd",
-                                    "kahan_fused", "winograd_fused"])
-def test_graph_replay_bitwise(method):
+@pytest.mark.parametrize("method,levels", [("naive", 0), ("kahan", 0), ("winograd", 0), ("winograd_scaled", 0),
+                                           ("strassen", 2), ("strassen_winograd", 2), ("strassen", 3),
+                                           ("strassen_winograd", 3), ("kahan_fused", 0), ("winograd_fused", 0)])
+def test_graph_replay_bitwise(method, levels):
     A, B = workload.custom(130, 98, 120, seed=4)
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    kw = {"levels": 2} if method.startswith("strassen") else {}
+    kw = {"levels": levels} if method.startswith("strassen") else {}
     direct = getattr(mm, method)(dA, dB, **kw).clone()
     g = mm.GraphedProduct(method, dA, dB, **kw)
     assert torch.equal(g.replay(), direct)
