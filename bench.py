@@ -135,13 +135,12 @@ def oracle_sample(cfg, A, B, levels, budget_s: float, methods, lam=None, counts=
     import numpy as np
 
     import oracle
-    import paper_1106_1347_b200 as mm
     import workload
 
     N, P, M = A.shape[0], A.shape[1], B.shape[1]
     if lam is None and "winograd_scaled" in methods:
         lam = oracle.lam(oracle.norm_inf(A), oracle.norm_inf(B))
-    d, Np, Pp, Mp = mm.strassen_plan(N, P, M, levels)
+    d, (Np, Pp, Mp) = oracle.plan(N, P, M, levels)
     pos = workload.sample_positions(cfg.cfg_id, N, M, 200000, shard=42)
     total_t, total_f, used = 0.0, 0.0, {}
     per_method = budget_s / len(methods)

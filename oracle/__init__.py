@@ -331,6 +331,14 @@ def _plan(N, P, M, levels, pad):
     return levels, tuple(int(x) for x in pad)
 
 
+def plan(N: int, P: int, M: int, levels: int):
+    """(depth, (Np, Pp, Mp)): the paper's square plan for levels < 0, else `levels` levels with
+    every dimension padded to a multiple of 2^(levels+1) (reading R10).  The same plan the library
+    computes (tests/test_abi_cpu.py pins the two equal); test and bench code takes it from here so
+    the oracle never depends on the product."""
+    return _plan(N, P, M, levels, None)
+
+
 def strassen(variant: int, A, B, levels=None, pad=None, base: int = BASE_LITERAL):
     """Strassen (variant 0) or Strassen-Winograd (variant 1).
 

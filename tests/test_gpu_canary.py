@@ -86,7 +86,7 @@ def _run(name, A, B, shift, levels, sampled):
     else:
         idx = [(i, j) for i in range(N) for j in range(M)]
     if variant is not None:
-        d, Np, Pp, Mp = mm.strassen_plan(N, P, M, levels)
+        d, (Np, Pp, Mp) = oracle.plan(N, P, M, levels)
         ref = oracle.entries_strassen(variant, A, B, idx, levels=d, pad=(Np, Pp, Mp), base=oracle.BASE_FMA)
     else:
         ref = oracle.entries(code, A, B, idx, int(lam.value))

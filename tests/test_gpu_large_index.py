@@ -42,7 +42,7 @@ def _gather(C: torch.Tensor, idx):
 
 def _reference(method, A, B, idx, levels):
     if method.startswith("strassen"):
-        d, Np, Pp, Mp = mm.strassen_plan(A.shape[0], A.shape[1], B.shape[1], levels)
+        d, (Np, Pp, Mp) = oracle.plan(A.shape[0], A.shape[1], B.shape[1], levels)
         return oracle.entries_strassen(0 if method == "strassen" else 1, A, B, idx, levels=d, pad=(Np, Pp, Mp),
                                        base=oracle.BASE_FMA)
     lam = oracle.lam(oracle.norm_inf(A), oracle.norm_inf(B)) if method == "winograd_scaled" else 0
