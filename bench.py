@@ -11,8 +11,14 @@ synthetic A, B.  Metric (BASELINE.json): FP64 GFLOP/s counted as 2NPM per method
 in "methods".
 
 N > 1 (torchrun, one process per GPU, NCCL): C is split by row blocks of A and B is broadcast
-from rank 0 inside every step (paper_1106_1347_b200.dist); the global problem is fixed, so
-scaling is "strong"; ms_per_step is the max over ranks.
+from rank 0 inside every product, following the library's multi-GPU schedule (mm_dist_schedule:
+B in row panels that the product consumes as they land) executed over torch.distributed
+(paper_1106_1347_b200.dist.dist_gemm -- the executor the two-rank CPU tests drive) or, with
+--dist-impl native, by the library's own NCCL layer (mm_dist_gemm).  The global problem is fixed,
+so scaling is "strong"; ms_per_step is the max over ranks.
+
+BASELINE.json's scaling config (c5, 32768^3, classical + Strassen-Winograd at 1/2/4/8 GPUs):
+    python bench.py --config c5 --methods naive,strassen_winograd --levels 2 [--gpus N]
 
 --impl reference times the CPU oracle (oracle/, the plain C99 implementation the parity tests
 use) on a bounded sample of entries of the same workload: this task has no runnable
@@ -58,11 +64,16 @@ def parse_args():
     ap.add_argument("--levels", type=int, default=3, help="Strassen recursion levels (c4: 3 levels, 1024^3 leaves, is fastest: profiles/r01/table_v2.jsonl)")
     ap.add_argument("--methods", default=",".join(METHODS))
     ap.add_argument("--panels", type=int, default=8,
-                    help="N>1: B broadcast in this many k-panels overlapped with NaivStandard's accumulation "
-                         "(NaivKahan / WinogradOriginal: half as many; their per-panel cost is higher, "
+                    help="N>1: B broadcast in this many row panels overlapped with NaivStandard's accumulation "
+                         "(the other methods: half as many; their per-panel cost is higher, "
                          "profiles/r01/panel_bench.jsonl)")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="N > 1 collectives (gloo only to exercise the multi-rank path on fewer GPUs)")
+    ap.add_argument("--dist-impl", default="torch", choices=("torch", "native"),
+                    help="N > 1 executor of the schedule: torch.distributed (dist.dist_gemm) or the library's "
+                         "own NCCL layer (mm_dist_gemm)")
+    ap.add_argument("--err-rows", type=int, default=2,
+                    help="rows of C checked against the exactly rounded product (abs_err column); 0 = off")
     ap.add_argument("--e2e-blocks", type=int, default=8,
                     help="e2e: k-panels / row blocks the host<->device copies are pipelined in")
     ap.add_argument("--no-e2e", action="store_true")
@@ -208,16 +219,56 @@ def run_reference(args):
     return 0
 
 
+def panels_for_method(args, m):
+    return args.panels if m == "naive" else max(1, args.panels // 2)
+
+
+def exact_rows(A_rows, B):
+    """Rows of the product AB to about twice double precision, as the reference of the
+    error column: Ogita-Rump-Oishi Dot2 -- every product split exactly into p + e (Dekker's
+    TwoProduct, 2^27 + 1 splitting), the p summed with TwoSum and every rounding error and e carried
+    in a second accumulator -- vectorised over the columns.  Its error is below u |(AB)_ij| +
+    (P u)^2 sum_k |A_ik B_kj| (u = 2^-53), orders of magnitude under any method's, so this stands
+    for the exact product of Brent's ||E||.  Diagnostic, outside the timed
+    region."""
+    import numpy as np
+
+    split = 134217729.0
+
+    def halves(x):
+        t = split * x
+        hi = t - (t - x)
+        return hi, x - hi
+
+    bh, bl = halves(B)
+    out = np.empty((A_rows.shape[0], B.shape[1]))
+    for r in range(A_rows.shape[0]):
+        s = np.zeros(B.shape[1])
+        c = np.zeros(B.shape[1])
+        for k in range(B.shape[0]):
+            a = float(A_rows[r, k])
+            p = a * B[k]
+            ah, al = halves(a)
+            e = ((ah * bh[k] - p) + ah * bl[k] + al * bh[k]) + al * bl[k]  # a B[k] = p + e exactly
+            t = s + p
+            z = t - s
+            c += ((s - (t - z)) + (p - z)) + e  # TwoSum error of s + p, plus e
+            s = t
+        out[r] = s + c
+    return out
+
+
 def config_dict(args, cfg, world):
     return {
         "workload": f"{cfg.key}: A {cfg.N}x{cfg.P}, B {cfg.P}x{cfg.M} float64 ({cfg.dist}), one call of each of "
                     f"{args.methods.replace(',', ', ')} per step",
         "N": cfg.N, "P": cfg.P, "M": cfg.M, "strassen_levels": args.levels,
-        "parallelism": (f"row-block dp{world} (B broadcast via {args.dist_backend}; k-panels overlapped: naive "
-                        f"{args.panels}, kahan / winograd {max(1, args.panels // 2)})"
+        "parallelism": (f"row-block dp{world} (B broadcast via {args.dist_backend}, schedule executed by "
+                        f"{'mm_dist_gemm' if args.dist_impl == 'native' else 'dist.dist_gemm'}; row panels "
+                        f"overlapped: naive {args.panels}, others {max(1, args.panels // 2)})"
                         if world > 1 else "1 GPU"),
-        "l2": "inputs larger than L2 (A, B, C = 537 MB each vs 126 MB L2)" if cfg.N >= 4096
-        else "inputs smaller than L2 (not flushed)",
+        "l2": (f"inputs larger than L2 (A, B, C = {8 * cfg.N * cfg.P / 1e6:.0f} MB each vs 126 MB L2)"
+               if cfg.N >= 4096 else "inputs smaller than L2 (not flushed)"),
     }
 
 
@@ -252,11 +303,12 @@ def run_mine(args):
     outs = {m: torch.empty((n_loc, M), dtype=torch.float64, device=dev) for m in methods}
     stream = torch.cuda.current_stream(dev)
 
-    # N > 1 over NCCL: the C ABI's own layer (mm_dist_*); over gloo: the torch.distributed driver
-    native = mmdist.NativeComm() if world > 1 and args.dist_backend == "nccl" else None
+    # N > 1: the library's schedule, executed over torch.distributed (default) or by the library's
+    # own NCCL layer (--dist-impl native)
+    native = mmdist.NativeComm() if world > 1 and args.dist_impl == "native" and args.dist_backend == "nccl" else None
 
     def panels_for(m):
-        return args.panels if m == "naive" else max(1, args.panels // 2)
+        return panels_for_method(args, m)
 
     def one_method(m):
         if native is not None:
@@ -337,6 +389,23 @@ def run_mine(args):
             entry["rel_err_vs_kahan"] = e / (nA * nB) if nA * nB > 0 else 0.0
         res[m] = entry
 
+    # ||E||_inf against the exactly rounded product on a few seeded rows of this rank's shard
+    # (Brent's E), as sum_j |C_ij - (AB)_ij| / (||A|| ||B||)
+    if args.err_rows > 0 and rank == 0 and n_loc > 0:
+        rows = sorted({int(i) for i in workload.sample_positions(cfg.cfg_id, n_loc, M, 64, shard=7)[:, 0]})
+        rows = rows[:args.err_rows]
+        cols = np.arange(M) if M <= 8192 else np.sort(workload.sample_positions(cfg.cfg_id, 1, M, 4096, 8)[:, 1])
+        X = exact_rows(A_h[rows], B_h[:, cols])
+        ii = torch.tensor(rows, device=dev)
+        jj = torch.from_numpy(cols).to(dev)
+        for m in methods:
+            Cm = outs[m][ii][:, jj].cpu().numpy()
+            res[m]["rel_err_vs_exact"] = float(np.abs(Cm - X).sum(axis=1).max()) / (nA * nB) if nA * nB > 0 else 0.0
+        err_note = (f"rows {rows} of rank 0's shard, {'all' if M <= 8192 else len(cols)} columns, "
+                    f"against the exactly rounded product (TwoProduct + fsum)")
+    else:
+        err_note = None
+
     # roofline of the dominant kernel (largest share of the step)
     traffic = load_traffic()
     n_eff = n_loc
@@ -373,6 +442,8 @@ def run_mine(args):
         "config": config_dict(args, cfg, world), "methods": res, "roofline": roofline,
         "roofline_by_kernel": roof_all, "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
     }
+    if err_note:
+        line["err_sample"] = err_note
     if rank == 0 and world == 1 and not args.no_cpu:
         f, t, used = oracle_sample(cfg, A_h, B_h, args.levels, args.cpu_seconds, methods)
         line["cpu_baseline"] = {
@@ -406,7 +477,15 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
     # a row-local method first (its row blocks start as A lands) and one last (its C streams back
     # by row blocks); the per-step work is the same six products as the device-timed step.
     order = sorted(methods, key=lambda m: {"naive": 0, "kahan": 9}.get(m, 5))
-    houts = {m: torch.empty((n_loc, M), dtype=torch.float64).pin_memory() for m in methods} if world == 1 else None
+    houts = None
+    if world == 1:
+        # one pinned host C per method; above 16 GB of them (c5) the methods share one (the copies are
+        # ordered on one copy stream, so each product still crosses PCIe in full every step)
+        if 8.0 * n_loc * M * len(methods) <= 16e9:
+            houts = {m: torch.empty((n_loc, M), dtype=torch.float64).pin_memory() for m in methods}
+        else:
+            shared = torch.empty((n_loc, M), dtype=torch.float64).pin_memory()
+            houts = {m: shared for m in methods}
 
     def step():
         if world == 1:
@@ -418,7 +497,7 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
         if rank == 0:
             dB.copy_(hB, non_blocking=True)
         for m in methods:
-            pn = args.panels if m == "naive" else max(1, args.panels // 2)
+            pn = panels_for_method(args, m)
             if native is not None:
                 C = native.gemm(m, dA, dB, levels=args.levels, panels=pn)
             else:
@@ -431,7 +510,7 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, args.steps)
     t0.record(stream)
     for _ in range(steps):
         step()

@@ -233,21 +233,65 @@ int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_
  *   current).  MM_ERR_ARG if already initialised or arguments are out of range.
  * mm_dist_gemm -- C_shard = A_shard B for this rank's N_local rows (N_local >= 0; a rank without
  *   rows still takes part in the collectives).  B: DEVICE buffer P x M on every rank; the root's
- *   content is broadcast into it in place inside the call.  method: an mm_method id.  For
- *   MM_NAIVE, MM_KAHAN[_FUSED] and MM_WINOGRAD[_FUSED] with panels > 1, B travels as `panels`
- *   (<= 64, even boundaries) row panels on the layer's own stream and the product accumulates
- *   panel by panel (mm_naive_ex / mm_kahan_ex with the carried err in the workspace /
- *   mm_winograd_ex, y and z of the full operands computed once the last panel has landed), each
- *   panel's step waiting only for its own transfer -- bitwise the one-shot product.  Kahan and
- *   Winograd take the panel path only for 16-byte aligned operands with P and M even (else one
- *   broadcast, then the one-shot kernel).  WinogradScaled uses the global
- *   ||A||_inf (max-all-reduce of the row blocks' norms) and the local ||B||_inf, so lambda equals
- *   the one-GPU lambda.  Classical, Kahan and both Winograds are bitwise the rows of the one-GPU
- *   product; Strassen recurses on the shard (within its tolerance).  workspace: DEVICE, >=
- *   mm_dist_workspace_size(...).  Stream-ordered and asynchronous like the other entry points;
- *   the current device must be the one given to mm_dist_init.
+ *   content is broadcast into it in place inside the call.  method: an mm_method id.  The call
+ *   executes the schedule mm_dist_schedule(method, P, M, levels, panels) returns: communication
+ *   ops in order on the layer's own stream, compute ops (mm_dist_step) in order on `stream`,
+ *   joined by events -- the same schedule the torch.distributed driver (paper_1106_1347_b200.dist)
+ *   executes.  The schedule depends only on (method, P, M, levels, panels), values every rank
+ *   shares, so every rank issues the same collectives.  Classical, Kahan and both Winograds are
+ *   bitwise the rows of the one-GPU product; Strassen recurses on the shard (within its
+ *   tolerance).  workspace: DEVICE, >= mm_dist_workspace_size(...).  Stream-ordered and
+ *   asynchronous like the other entry points; the current device must be the one given to
+ *   mm_dist_init.
  * mm_dist_finalize -- destroy the communicator and the layer's stream and events.
+ *
+ * mm_dist_schedule -- the multi-GPU schedule of one product as a list of ops (HOST array `ops` of
+ *   `cap` entries; returns the number of ops, or MM_ERR_ARG for bad arguments / a too small cap --
+ *   16 + 12 * panels always suffices).  Pure host function (no GPU).  Ops:
+ *     MM_OP_BCAST            comm: broadcast rows [lo, hi) of B from the root
+ *     MM_OP_ALLREDUCE_NORMS  comm: max-all-reduce of the two doubles at the workspace start
+ *     MM_OP_RECORD / _WAIT   record / wait for event `index` on `stream` (MM_STREAM_*)
+ *     MM_OP_NORMS .. _FULL   compute ops, run by mm_dist_step (below) in list order.
+ *   With panels > 1 B travels as row panels and the product follows panel by panel (SURVEY 8(f)
+ *   NEXT-4): NaivStandard, NaivKahan and WinogradOriginal (+ fused) accumulate k-panels
+ *   (mm_naive_ex / mm_kahan_ex / mm_winograd_ex, Kahan/Winograd when P and M are even);
+ *   WinogradScaled (P and M even) max-all-reduces {||A_r||, ||B|| of the root} before B moves, so
+ *   lambda is known at once, then scales each arriving panel of B (z' continued panel to panel)
+ *   and accumulates its pair sums; Strassen (levels >= 1) forms the B-side operands of each
+ *   arriving panel -- panel i is the quadrant rows [u_i, u_{i+1}) of the first formation pass,
+ *   i.e. the B rows u + r (Pp >> s), r < 2^s, s the levels that pass spans.  Otherwise (panels
+ *   <= 1, odd P or M, the paper plan levels = -1): one broadcast, then the one-GPU method.
+ *   Panels are listed in increasing k, so every result is bitwise the one-broadcast schedule's.
+ * mm_dist_step -- run ONE compute op of a schedule on `stream` (no communication): A_shard, B,
+ *   C_shard, workspace as for mm_dist_gemm; is_root: this rank is the broadcast root (MM_OP_NORMS
+ *   then contributes ||B||, other ranks 0).  B rows an op reads must already hold the root's data
+ *   (the schedule's WAIT ops ensure it).  A rank whose operands cannot use the panel kernels (an
+ *   A_shard that is not 16-byte aligned) skips the panel steps and runs the one-GPU kernel at the
+ *   last one -- its collectives are unchanged.  N_local == 0: every op but MM_OP_NORMS is a no-op.
  */
+#define MM_OP_BCAST 1
+#define MM_OP_ALLREDUCE_NORMS 2
+#define MM_OP_RECORD 3
+#define MM_OP_WAIT 4
+#define MM_OP_NORMS 5        /* ||A_r||_inf -> norms[0]; root: ||B||_inf -> norms[1], else 0 */
+#define MM_OP_PANEL 6        /* k-panel [lo, hi) with MM_EX_* flags (scaled: on 2^lambda A, 2^-lambda B) */
+#define MM_OP_YZ 7           /* WinogradOriginal's y, z of the full operands (before its last panel) */
+#define MM_OP_SCALE_A 8      /* lambda from the norms; 2^lambda A and its y' */
+#define MM_OP_SCALE_B 9      /* rows [lo, hi) of 2^-lambda B, z' continued (flags & MM_EX_ACCUMULATE) */
+#define MM_OP_FORM_A 10      /* Strassen: every A-side formation pass */
+#define MM_OP_FORM_B 11      /* Strassen: the first B-side pass on its units [lo, hi) */
+#define MM_OP_FORM_B_REST 12 /* Strassen: the remaining B-side passes */
+#define MM_OP_LEAF_COMBINE 13 /* Strassen: the batched leaf products and the combination passes */
+#define MM_OP_FULL 14        /* the one-GPU method on the shard (B complete) */
+#define MM_STREAM_COMPUTE 0
+#define MM_STREAM_COMM 1
+typedef struct {
+  int32_t op;     /* MM_OP_* */
+  int32_t stream; /* MM_STREAM_* (RECORD / WAIT) */
+  int32_t index;  /* event slot (RECORD / WAIT), panel number (other ops) */
+  int32_t flags;  /* MM_EX_* (PANEL, SCALE_B) */
+  int64_t lo, hi; /* row range of B (BCAST, SCALE_B), k range (PANEL), unit range (FORM_B) */
+} mm_dist_op;
 int mm_dist_get_unique_id(void* id_out);
 int mm_dist_init(int32_t rank, int32_t world, const void* unique_id, int32_t device);
 size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M, int32_t levels);
@@ -255,6 +299,10 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
                  int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
                  void* stream);
 int mm_dist_finalize(void);
+int mm_dist_schedule(int method, int64_t P, int64_t M, int32_t levels, int32_t panels, mm_dist_op* ops, int32_t cap);
+int mm_dist_step(int method, const mm_dist_op* op, const double* A_shard, const double* B, double* C_shard,
+                 int64_t N_local, int64_t P, int64_t M, int32_t levels, int32_t is_root, void* workspace,
+                 size_t ws_bytes, void* stream);
 
 /*
  * mm_launch_count -- number of kernels this library has launched in this process (a

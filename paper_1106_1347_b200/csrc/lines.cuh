@@ -10,7 +10,9 @@
 // The sums must run in index order (reading R1/R17: the oracle's order; on ill-scaled inputs
 // a different order changes y by ~50, SURVEY PR-7), so one lane owns one line and there is no
 // parallelism inside a line.  The kernel is therefore built to keep HBM busy with few warps:
-//   * one warp = 32 lines, one warp per CTA, a LN_STAGES-deep shared-memory ring of
+//   * one warp = 32 lines, one warp per CTA, a shared-memory ring of LN_STAGES (6) to
+//     LN_MAX_STAGES (24) stages -- deeper when the grid leaves SMs to spare (a 1024-row shard of
+//     A is only 32 warps: each then keeps 24 x 8 KB in flight instead of 6 x 8 KB) -- of
 //     32 x LN_TK tiles;
 //   * operands with a 16-byte aligned base and even pitch arrive by TMA (2-D tensor maps,
 //     one elected lane issues the tile's box copies, completion counted in bytes on an
@@ -23,15 +25,26 @@
 //     rounding as the oracle's copy), so WinogradScaled needs one pass over A and B after
 //     the norms instead of copy + y/z passes.
 // Up to two jobs (e.g. rows of A and columns of B) share one launch.
+//
+// K4 norm_inf: one lane per row, the row summed left to right (bitwise the oracle's row sums); the
+// max over rows is order-free: each warp reduces its 32 rows and issues one atomicMax on the IEEE
+// bit pattern (non-negative doubles order like their uint64 images; a NaN row sum is forced to the
+// canonical quiet NaN, whose pattern exceeds +inf's, so it propagates).  K5, the lambda rule
+// (lambda_rule below), is evaluated on the device by every block of the scaled pass from the two
+// norms K4 left in device memory -- no host round trip and no separate launch.
 #pragma once
+#include <cstdlib>
+
 #include "tma.cuh"
 
 namespace mmk {
 
-constexpr int LN_LINES = 32, LN_TK = 32, LN_STAGES = 6;
+constexpr int LN_LINES = 32, LN_TK = 32, LN_STAGES = 6, LN_MAX_STAGES = 24;
 constexpr int LN_TILE = LN_LINES * LN_TK;  // 8 KB per stage
 constexpr unsigned LN_TILE_BYTES = LN_TILE * sizeof(double);
-constexpr size_t LN_SMEM = 1024 + size_t(LN_STAGES) * LN_TILE * sizeof(double) + LN_STAGES * sizeof(uint64_t);
+inline constexpr size_t ln_smem(int stages) {
+  return 1024 + size_t(stages) * LN_TILE * sizeof(double) + stages * sizeof(uint64_t);
+}
 static_assert(LN_TK == 32 && LN_LINES == 32, "one lane per tile column / line");
 
 // LN_PAIRS_FMA: the NEXT-3 fused variant (reading R22), y = fma(x0, x1, y)
@@ -49,6 +62,8 @@ struct LineJob {
   int64_t len;                   // elements streamed per line (columns, or rows)
   int64_t pair_end;              // LN_PAIRS: only elements < pair_end enter the sum (2 floor(P/2))
   double* out;                   // LN_PAIRS: per-line sums
+  const double* init;            // LN_PAIRS, optional: per-line start values (a sum continued over a
+                                 // later row panel of B -- the multi-GPU scaled Winograd, mm_dist_step)
   unsigned long long* out_max;   // LN_ABS: max over lines, as the bit pattern of a non-negative double
   double* copy;                  // optional scaled copy (same shape and ld as X)
   int by_rows;
@@ -63,6 +78,7 @@ struct LineLaunch {
   LineJob job[2];
   int njobs;
   const unsigned long long* norms;  // {||A||, ||B||} bit patterns (for scale_sel >= 0)
+  int stages;                       // ring depth (LN_STAGES .. LN_MAX_STAGES), set by launch_lines
   int* lam_out;                     // optional: lambda, written by block 0
   double* scale_out;                // optional: {2^lambda, 2^-lambda}, written by block 0
 };
@@ -131,7 +147,8 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   extern __shared__ __align__(1024) unsigned char ln_raw[];
   // 1024-byte aligned stage buffers (the 128-byte swizzle pattern repeats every 1024 bytes)
   double* ln_smem = reinterpret_cast<double*>(ln_raw + ((1024 - (smem_u32(ln_raw) & 1023)) & 1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ln_smem + LN_STAGES * LN_TILE);
+  const int S = L.stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ln_smem + S * LN_TILE);
   const int lane = threadIdx.x;
   int b = blockIdx.x, ji = 0;
   if (L.njobs > 1 && b >= L.job[0].blocks) {
@@ -159,33 +176,33 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
 
   if (lane == 0) {
     if (jb.bulk) tma_prefetch_desc(&L.map[ji]);
-    for (int st = 0; st < LN_STAGES; ++st) mbar_init(bars + st, jb.bulk ? 1 : LN_LINES);
+    for (int st = 0; st < S; ++st) mbar_init(bars + st, jb.bulk ? 1 : LN_LINES);
     fence_mbar_init();
   }
   __syncwarp();
 #pragma unroll 1
-  for (int st = 0; st < LN_STAGES; ++st)
+  for (int st = 0; st < S; ++st)
     if (st < KT) ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, st, lane);
 
   const bool scaled = SCALED && jb.scale_sel >= 0;
-  double acc = 0.0;
+  double acc = (OP != LN_ABS && jb.init && l0 + lane < jb.nlines) ? jb.init[l0 + lane] : 0.0;
 #pragma unroll 1
   for (int64_t kt = 0; kt < KT; ++kt) {
     if (kt >= 1) {
       // refill tile kt-1's stage with tile kt-1+STAGES here, after the loop back edge: every op
       // consuming its shared-memory loads has issued, so those loads have completed (refilling
       // at the end of iteration kt-1 would let ptxas hoist the copy above in-flight loads)
-      const int64_t nk = kt - 1 + LN_STAGES;
+      const int64_t nk = kt - 1 + S;
       if (jb.bulk) fence_proxy_async_smem();
       __syncwarp();
       if (nk < KT) {
-        const int sp = int((kt - 1) % LN_STAGES);
+        const int sp = int((kt - 1) % S);
         ln_issue(L, ji, ln_smem + sp * LN_TILE, bars + sp, l0, nk, lane);
       }
       __syncwarp();
     }
-    const int st = int(kt % LN_STAGES);
-    mbar_wait(bars + st, unsigned((kt / LN_STAGES) & 1));
+    const int st = int(kt % S);
+    mbar_wait(bars + st, unsigned((kt / S) & 1));
     const double* t = ln_smem + st * LN_TILE;
     const int64_t k0 = kt * LN_TK;
     const int kv = int(jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK);
@@ -269,9 +286,12 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   const bool valid = l0 + lane < jb.nlines;
   if (OP == LN_ABS) {
     double m = valid ? acc : 0.0;  // max is order-free
+    const bool any_nan = __any_sync(0xffffffffu, valid && isnan(acc));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) atomicMax(jb.out_max, static_cast<unsigned long long>(__double_as_longlong(m)));
+    const unsigned long long bits =
+        any_nan ? 0x7ff8000000000000ull : static_cast<unsigned long long>(__double_as_longlong(m));
+    if (lane == 0) atomicMax(jb.out_max, bits);
   } else {
     if (valid) jb.out[l0 + lane] = acc;
   }
@@ -292,14 +312,32 @@ inline void ln_finish_job(LineJob& j, CUtensorMap* map) {
 
 template <int OP, bool SCALED = false>
 inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
-  cudaError_t e = smem_attr_once<line_kernel<OP, SCALED>>(LN_SMEM);
+  cudaError_t e = smem_attr_once<line_kernel<OP, SCALED>>(ln_smem(LN_MAX_STAGES));
   if (e != cudaSuccess) return e;
   int blocks = 0;
   for (int i = 0; i < L.njobs; ++i) {
     ln_finish_job(L.job[i], &L.map[i]);
     blocks += L.job[i].blocks;
   }
-  line_kernel<OP, SCALED><<<unsigned(blocks), LN_LINES, LN_SMEM, st>>>(L);
+  // ring depth: the shared memory of an SM (~220 KB usable) shared by the blocks it will hold
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                   cudaSuccess) {
+      cudaGetLastError();
+      sms = 148;
+    }
+  }
+  const int per_sm = int((blocks + sms - 1) / sms);
+  int stages = int((220 * 1024 / (per_sm > 0 ? per_sm : 1) - 1024) / (LN_TILE * sizeof(double) + 8));
+  static const int cap = [] {  // MM_LN_MAX_STAGES: tuning override of the depth cap (6 .. 24)
+    const char* e = std::getenv("MM_LN_MAX_STAGES");
+    const int v = e ? std::atoi(e) : LN_MAX_STAGES;
+    return v < LN_STAGES ? LN_STAGES : (v > LN_MAX_STAGES ? LN_MAX_STAGES : v);
+  }();
+  L.stages = stages < LN_STAGES ? LN_STAGES : (stages > cap ? cap : stages);
+  line_kernel<OP, SCALED><<<unsigned(blocks), LN_LINES, ln_smem(L.stages), st>>>(L);
   note_launch();
   return cudaGetLastError();
 }
@@ -334,6 +372,12 @@ inline cudaError_t launch_norms(const double* X0, int64_t r0, int64_t c0, const 
   return launch_lines<LN_ABS>(L, st);
 }
 
+// out: device uint64 slot, zeroed here then max-reduced
+inline cudaError_t launch_norm_inf(const double* X, int64_t rows, int64_t cols, unsigned long long* out,
+                                   cudaStream_t st) {
+  return launch_norms(X, rows, cols, nullptr, 0, 0, out, st);
+}
+
 // Winograd y (rows of A) and z (columns of B); optionally on the exact scaled copies
 // As = 2^lambda A, Bs = 2^-lambda B, which are written in the same pass (lambda from norms).
 inline cudaError_t launch_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M,
@@ -361,6 +405,40 @@ inline cudaError_t launch_yz(const double* A, const double* B, double* y, double
   }
   if (scaled) return fused ? launch_lines<LN_PAIRS_FMA, true>(L, st) : launch_lines<LN_PAIRS, true>(L, st);
   return fused ? launch_lines<LN_PAIRS_FMA, false>(L, st) : launch_lines<LN_PAIRS, false>(L, st);
+}
+
+// The two halves of launch_yz's scaled pass, for the multi-GPU WinogradScaled (mm_dist_step):
+// MM_OP_SCALE_A: As = 2^lambda A and y' (rows of A); MM_OP_SCALE_B: rows [k0, k1) of Bs = 2^-lambda B
+// and z' continued over those rows (k0 even; `chain` = continue z' from its current value, else start
+// at 0).  Panels in increasing k0 perform every z'_k's operations in the one-pass order, so y', z'
+// and the copies are bitwise those of launch_yz(..., As, Bs, ...).
+inline cudaError_t launch_scale_rows(const double* A, double* As, double* y, int64_t N, int64_t P,
+                                     const unsigned long long* norms, cudaStream_t st, bool fused) {
+  LineLaunch L{};
+  L.njobs = 1;
+  L.norms = norms;
+  L.job[0] = ln_job(A, P, N, P, true, LN_PAIRS);
+  L.job[0].pair_end = 2 * (P / 2);
+  L.job[0].out = y;
+  L.job[0].copy = As;
+  L.job[0].scale_sel = 0;
+  return fused ? launch_lines<LN_PAIRS_FMA, true>(L, st) : launch_lines<LN_PAIRS, true>(L, st);
+}
+
+inline cudaError_t launch_scale_cols(const double* B, double* Bs, double* z, int64_t P, int64_t M, int64_t k0,
+                                     int64_t k1, bool chain, const unsigned long long* norms, cudaStream_t st,
+                                     bool fused) {
+  LineLaunch L{};
+  L.njobs = 1;
+  L.norms = norms;
+  L.job[0] = ln_job(B + k0 * M, M, M, k1 - k0, false, LN_PAIRS);
+  const int64_t pe = 2 * (P / 2) - k0;
+  L.job[0].pair_end = pe < k1 - k0 ? pe : k1 - k0;
+  L.job[0].out = z;
+  L.job[0].init = chain ? z : nullptr;
+  L.job[0].copy = Bs + k0 * M;
+  L.job[0].scale_sel = 1;
+  return fused ? launch_lines<LN_PAIRS_FMA, true>(L, st) : launch_lines<LN_PAIRS, true>(L, st);
 }
 
 }  // namespace mmk

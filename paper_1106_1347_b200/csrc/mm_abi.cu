@@ -12,7 +12,7 @@
 #include "dist_nccl.cuh"
 #include "gemm_tma.cuh"
 #include "kahan.cuh"
-#include "norm_lambda.cuh"
+#include "lines.cuh"
 #include "strassen.cuh"
 #include "winograd.cuh"
 
@@ -379,9 +379,10 @@ int mm_dist_init(int32_t rank, int32_t world, const void* unique_id, int32_t dev
     return MM_ERR_NCCL;
   }
   cudaError_t e = cudaStreamCreateWithFlags(&ds.comm_stream, cudaStreamNonBlocking);
-  for (int i = 0; e == cudaSuccess && i < mmk::DistState::kMaxPanels; ++i)
+  for (int i = 0; e == cudaSuccess && i < mmk::kDistEvents; ++i)
     e = cudaEventCreateWithFlags(&ds.panel_ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ds.start_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ds.end_ev, cudaEventDisableTiming);
   ds.rank = rank;
   ds.world = world;
   ds.device = device;
@@ -394,9 +395,10 @@ int mm_dist_finalize(void) {
   mmk::NcclApi* api = mmk::nccl_api();
   const ncclResult_t r = api->CommDestroy(ds.comm);
   if (ds.comm_stream) cudaStreamDestroy(ds.comm_stream);
-  for (int i = 0; i < mmk::DistState::kMaxPanels; ++i)
+  for (int i = 0; i < mmk::kDistEvents; ++i)
     if (ds.panel_ev[i]) cudaEventDestroy(ds.panel_ev[i]);
   if (ds.start_ev) cudaEventDestroy(ds.start_ev);
+  if (ds.end_ev) cudaEventDestroy(ds.end_ev);
   ds = mmk::DistState();
   return r == ncclSuccess ? MM_OK : MM_ERR_NCCL;
 }
@@ -412,6 +414,119 @@ size_t mm_dist_workspace_size(int method, int64_t N_local, int64_t P, int64_t M,
   return mm_workspace_size(method, n, P, M, levels);
 }
 
+int mm_dist_schedule(int method, int64_t P, int64_t M, int32_t levels, int32_t panels, mm_dist_op* ops,
+                     int32_t cap) {
+  const int n = mmk::build_dist_schedule(method, P, M, levels, panels, ops, cap);
+  return n < 0 ? MM_ERR_ARG : n;
+}
+
+int mm_dist_step(int method, const mm_dist_op* op, const double* A, const double* B, double* C, int64_t N,
+                 int64_t P, int64_t M, int32_t levels, int32_t is_root, void* workspace, size_t ws_bytes,
+                 void* stream) {
+  if (!op || !B || P < 1 || M < 1 || N < 0 || method < MM_NAIVE || method > MM_WINOGRAD_SCALED_FUSED)
+    return MM_ERR_ARG;
+  if (N > 0 && (!A || !C)) return MM_ERR_ARG;
+  if (!mul_ok(P, M) || (N > 0 && (!mul_ok(N, P) || !mul_ok(N, M)))) return MM_ERR_ARG;
+  const size_t need = mm_dist_workspace_size(method, N, P, M, levels);
+  if (need > 0 && (!workspace || ws_bytes < need)) return MM_ERR_WORKSPACE;
+  int sms = 148;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  mmk::NvtxRange nvtx("mm_dist_step");
+  cudaStream_t st = S(stream);
+  const bool scaled = method == MM_WINOGRAD_SCALED || method == MM_WINOGRAD_SCALED_FUSED;
+  const bool kahan = method == MM_KAHAN || method == MM_KAHAN_FUSED;
+  const bool wino = method == MM_WINOGRAD || method == MM_WINOGRAD_FUSED;
+  const bool strassen = method == MM_STRASSEN || method == MM_STRASSEN_WINOGRAD;
+  const bool fused = method == MM_KAHAN_FUSED || method == MM_WINOGRAD_FUSED || method == MM_WINOGRAD_SCALED_FUSED;
+  char* ws = static_cast<char*>(workspace);
+  auto* norms = reinterpret_cast<unsigned long long*>(ws);  // scaled: the (all-reduced) {||A||, ||B||}
+  if (op->op == MM_OP_NORMS) {
+    if (!scaled) return MM_ERR_ARG;
+    cudaError_t e = cudaMemsetAsync(norms, 0, 2 * sizeof(double), st);
+    mmk::LineLaunch L{};
+    if (N > 0) {
+      L.job[L.njobs] = mmk::ln_job(A, P, N, P, true, mmk::LN_ABS);
+      L.job[L.njobs++].out_max = norms;
+    }
+    if (is_root) {
+      L.job[L.njobs] = mmk::ln_job(B, M, P, M, true, mmk::LN_ABS);
+      L.job[L.njobs++].out_max = norms + 1;
+    }
+    if (e == cudaSuccess && L.njobs > 0) e = mmk::launch_lines<mmk::LN_ABS>(L, st);
+    return cuda_status(e);
+  }
+  if (N == 0) return MM_OK;  // a rank without rows only contributes to the collectives
+  // scaled layout: dist header (norms) | header | y' | z' | 2^lambda A | 2^-lambda B (scaled_ws)
+  char* sw = ws + kDistHeader;
+  double* ys = reinterpret_cast<double*>(sw + kScaledHeader);
+  double* zs = reinterpret_cast<double*>(sw + kScaledHeader + mmk::align256(size_t(N) * 8));
+  double* As = reinterpret_cast<double*>(sw + kScaledHeader + winograd_ws(N, M));
+  double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(P) * 8));
+  // Winograd: y | z; Kahan: the carried err E
+  double* y = reinterpret_cast<double*>(ws);
+  double* z = reinterpret_cast<double*>(ws + mmk::align256(size_t(N) * 8));
+  const int64_t lo = op->lo, hi = op->hi;
+  switch (op->op) {
+    case MM_OP_PANEL: {
+      if (lo < 0 || hi > P || lo >= hi || (lo & 1)) return MM_ERR_ARG;
+      const bool last = !(op->flags & MM_EX_KEEP_STATE);
+      if (method == MM_NAIVE)
+        return mm_naive_ex(A + lo, P, B + lo * M, M, C, M, N, hi - lo, M, (op->flags & MM_EX_ACCUMULATE) ? 1 : 0,
+                           stream);
+      if (!(kahan || wino || scaled)) return MM_ERR_ARG;
+      const double* Ao = scaled ? As : A;
+      const double* Bo = scaled ? Bs : B;
+      if (!mmk::simt_tma_ex_ok(Ao, P, Bo, M, N, P, M)) {
+        // this rank's operands cannot take the panel kernels: the one-GPU kernel once B is complete
+        if (!last) return MM_OK;
+        if (scaled)
+          return winograd_scaled_common(fused, A, B, C, N, P, M, reinterpret_cast<const double*>(norms), sw,
+                                        ws_bytes - kDistHeader, nullptr, stream);
+        return mm_gemm(method, A, B, C, N, P, M, levels, workspace, ws_bytes, nullptr, stream);
+      }
+      if (kahan)
+        return mm_kahan_ex(A + lo, P, B + lo * M, M, C, reinterpret_cast<double*>(ws), N, hi - lo, M, op->flags,
+                           stream);
+      return mm_winograd_ex(Ao + lo, P, Bo + lo * M, M, C, scaled ? ys : y, scaled ? zs : z, N, hi - lo, M,
+                            op->flags, stream);
+    }
+    case MM_OP_YZ:
+      if (!wino) return MM_ERR_ARG;
+      if (!mmk::simt_tma_ex_ok(A, P, B, M, N, P, M)) return MM_OK;  // the one-shot kernel makes its own
+      return mm_winograd_yz(A, B, N, P, M, y, z, fused ? MM_EX_FUSED : 0, stream);
+    case MM_OP_SCALE_A:
+      if (!scaled) return MM_ERR_ARG;
+      return cuda_status(mmk::launch_scale_rows(A, As, ys, N, P, norms, st, fused));
+    case MM_OP_SCALE_B:
+      if (!scaled || lo < 0 || hi > P || lo >= hi || (lo & 1)) return MM_ERR_ARG;
+      return cuda_status(
+          mmk::launch_scale_cols(B, Bs, zs, P, M, lo, hi, (op->flags & MM_EX_ACCUMULATE) != 0, norms, st, fused));
+    case MM_OP_FORM_A:
+    case MM_OP_FORM_B:
+    case MM_OP_FORM_B_REST:
+    case MM_OP_LEAF_COMBINE: {
+      if (!strassen) return MM_ERR_ARG;
+      mmk::StrassenPlan pl;
+      if (!mmk::make_strassen_plan(N, P, M, levels, &pl)) return MM_ERR_ARG;
+      const int ph = op->op == MM_OP_FORM_A   ? mmk::SP_FORM_A
+                     : op->op == MM_OP_FORM_B ? mmk::SP_FORM_B_FIRST
+                     : op->op == MM_OP_FORM_B_REST ? mmk::SP_FORM_B_REST
+                                                   : mmk::SP_LEAF_COMBINE;
+      const int64_t u0 = op->op == MM_OP_FORM_B ? lo : 0, u1 = op->op == MM_OP_FORM_B ? hi : INT64_MAX;
+      return cuda_status(method == MM_STRASSEN
+                             ? mmk::run_strassen<mmk::SV_NAIV>(A, B, C, N, P, M, pl, ws, sms, st, ph, u0, u1)
+                             : mmk::run_strassen<mmk::SV_WINOGRAD>(A, B, C, N, P, M, pl, ws, sms, st, ph, u0, u1));
+    }
+    case MM_OP_FULL:
+      if (scaled)
+        return winograd_scaled_common(fused, A, B, C, N, P, M, reinterpret_cast<const double*>(norms), sw,
+                                      ws_bytes - kDistHeader, nullptr, stream);
+      return mm_gemm(method, A, B, C, N, P, M, levels, workspace, ws_bytes, nullptr, stream);
+    default: return MM_ERR_ARG;
+  }
+}
+
 int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, int64_t N_local, int64_t P,
                  int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
                  void* stream) {
@@ -420,75 +535,59 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
   if (!ds.comm || !B || P < 1 || M < 1 || N_local < 0 || root < 0 || root >= ds.world) return MM_ERR_ARG;
   if (N_local > 0 && (!A_shard || !C_shard)) return MM_ERR_ARG;
   if (!mul_ok(P, M) || (N_local > 0 && (!mul_ok(N_local, P) || !mul_ok(N_local, M)))) return MM_ERR_ARG;
-  if (ws_bytes < mm_dist_workspace_size(method, N_local, P, M, levels)) return MM_ERR_WORKSPACE;
+  const size_t need = mm_dist_workspace_size(method, N_local, P, M, levels);
+  if (need > 0 && (!workspace || ws_bytes < need)) return MM_ERR_WORKSPACE;
   int dev = -1;
   if (cudaGetDevice(&dev) != cudaSuccess || dev != ds.device) return MM_ERR_ARG;
+  // the schedule depends only on (method, P, M, levels, panels): every rank issues the same collectives
+  static thread_local mm_dist_op ops[1024];
+  const int n = mmk::build_dist_schedule(method, P, M, levels, panels, ops, 1024);
+  if (n < 0) return MM_ERR_ARG;
   mmk::NcclApi* api = mmk::nccl_api();
-  cudaStream_t st = S(stream);
-  const size_t count = size_t(P) * size_t(M);
-  const bool kahan = method == MM_KAHAN || method == MM_KAHAN_FUSED;
-  const bool wino = method == MM_WINOGRAD || method == MM_WINOGRAD_FUSED;
-  const bool fused = method == MM_KAHAN_FUSED || method == MM_WINOGRAD_FUSED;
-  // the panel steps of Kahan / Winograd need the TMA-fed kernels (16-byte aligned, P and M even);
-  // other operands take the one-broadcast path below
-  const bool panel_ok = method == MM_NAIVE ||
-                        ((kahan || wino) && (N_local == 0 || mmk::simt_tma_ex_ok(A_shard, P, B, M, N_local, P, M)) &&
-                         P % 2 == 0 && M % 2 == 0);
-  if (panels > 1 && panel_ok) {
-    // NEXT-4: panel i of B crosses NVLink on the comm stream while panel i-1 is multiplied; every
-    // entry's running state (DMMA chain / Kahan (sum, err) / Winograd pair sum) continues from
-    // panel to panel in k order, so the shard is bitwise the one-shot product
-    int64_t bounds[mmk::DistState::kMaxPanels + 1];
-    const int np = mmk::dist_panel_bounds(P, panels, bounds);
-    cudaError_t e = cudaEventRecord(ds.start_ev, st);  // B may be rewritten once prior work on st is done
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds.comm_stream, ds.start_ev, 0);
-    if (e != cudaSuccess) return cuda_status(e);
-    for (int i = 0; i < np; ++i) {
-      double* Bp = B + bounds[i] * M;
-      if (api->Broadcast(Bp, Bp, size_t(bounds[i + 1] - bounds[i]) * size_t(M), ncclFloat64, root, ds.comm,
-                         ds.comm_stream) != ncclSuccess)
-        return MM_ERR_NCCL;
-      if ((e = cudaEventRecord(ds.panel_ev[i], ds.comm_stream)) != cudaSuccess) return cuda_status(e);
-    }
-    double* E = static_cast<double*>(workspace);  // Kahan: the carried err
-    double* y = static_cast<double*>(workspace);  // Winograd: y, z of the full operands
-    double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N_local) * 8));
-    const int32_t fx = fused ? MM_EX_FUSED : 0;
-    for (int i = 0; i < np; ++i) {
-      if ((e = cudaStreamWaitEvent(st, ds.panel_ev[i], 0)) != cudaSuccess) return cuda_status(e);
-      if (N_local == 0) continue;
-      const int64_t k0 = bounds[i], kw = bounds[i + 1] - bounds[i];
-      const bool last = i == np - 1;
-      const int32_t fl = fx | (i > 0 ? MM_EX_ACCUMULATE : 0) | (last ? 0 : MM_EX_KEEP_STATE);
-      int rc;
-      if (kahan) {
-        rc = mm_kahan_ex(A_shard + k0, P, B + k0 * M, M, C_shard, E, N_local, kw, M, fl, stream);
-      } else if (wino) {
-        if (last && (rc = mm_winograd_yz(A_shard, B, N_local, P, M, y, z, fx, stream))) return rc;
-        rc = mm_winograd_ex(A_shard + k0, P, B + k0 * M, M, C_shard, y, z, N_local, kw, M, fl, stream);
-      } else {
-        rc = mm_naive_ex(A_shard + k0, P, B + k0 * M, M, C_shard, M, N_local, kw, M, i > 0 ? 1 : 0, stream);
+  cudaStream_t st = S(stream), cs = ds.comm_stream;
+  cudaError_t e = cudaEventRecord(ds.start_ev, st);  // B may be rewritten once prior work on st is done
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ds.start_ev, 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  bool grouped = false;  // the broadcasts of one panel (Strassen: 2^span row ranges) are one NCCL group
+  for (int k = 0; k < n; ++k) {
+    const mm_dist_op& o = ops[k];
+    cudaStream_t os = o.stream == MM_STREAM_COMM ? cs : st;
+    switch (o.op) {
+      case MM_OP_BCAST: {
+        const bool more = k + 1 < n && ops[k + 1].op == MM_OP_BCAST && ops[k + 1].index == o.index;
+        if (more && !grouped) {
+          if (api->GroupStart() != ncclSuccess) return MM_ERR_NCCL;
+          grouped = true;
+        }
+        double* Bp = B + o.lo * M;
+        if (api->Broadcast(Bp, Bp, size_t(o.hi - o.lo) * size_t(M), ncclFloat64, root, ds.comm, cs) != ncclSuccess)
+          return MM_ERR_NCCL;
+        if (grouped && !more) {
+          if (api->GroupEnd() != ncclSuccess) return MM_ERR_NCCL;
+          grouped = false;
+        }
+        break;
       }
-      if (rc) return rc;
+      case MM_OP_ALLREDUCE_NORMS:
+        if (api->AllReduce(workspace, workspace, 2, ncclFloat64, ncclMax, ds.comm, cs) != ncclSuccess)
+          return MM_ERR_NCCL;
+        break;
+      case MM_OP_RECORD:
+        if ((e = cudaEventRecord(ds.panel_ev[o.index], os)) != cudaSuccess) return cuda_status(e);
+        break;
+      case MM_OP_WAIT:
+        if ((e = cudaStreamWaitEvent(os, ds.panel_ev[o.index], 0)) != cudaSuccess) return cuda_status(e);
+        break;
+      default: {
+        const int rc = mm_dist_step(method, &o, A_shard, B, C_shard, N_local, P, M, levels, ds.rank == root ? 1 : 0,
+                                    workspace, ws_bytes, stream);
+        if (rc) return rc;
+      }
     }
-    return MM_OK;
   }
-  if (api->Broadcast(B, B, count, ncclFloat64, root, ds.comm, st) != ncclSuccess) return MM_ERR_NCCL;
-  if (method == MM_WINOGRAD_SCALED || method == MM_WINOGRAD_SCALED_FUSED) {
-    // global ||A|| = max over the row blocks (order-free, exact); ||B|| is local (B replicated)
-    auto* norms = static_cast<unsigned long long*>(workspace);
-    cudaError_t e = N_local > 0 ? mmk::launch_norm_inf(A_shard, N_local, P, norms, st)
-                                : cudaMemsetAsync(norms, 0, sizeof(double), st);
-    if (e != cudaSuccess) return cuda_status(e);
-    if (api->AllReduce(norms, norms, 1, ncclFloat64, ncclMax, ds.comm, st) != ncclSuccess) return MM_ERR_NCCL;
-    if ((e = mmk::launch_norm_inf(B, P, M, norms + 1, st)) != cudaSuccess) return cuda_status(e);
-    if (N_local == 0) return MM_OK;
-    return winograd_scaled_common(method == MM_WINOGRAD_SCALED_FUSED, A_shard, B, C_shard, N_local, P, M,
-                                  reinterpret_cast<const double*>(norms), static_cast<char*>(workspace) + kDistHeader,
-                                  ws_bytes - kDistHeader, nullptr, stream);
-  }
-  if (N_local == 0) return MM_OK;
-  return mm_gemm(method, A_shard, B, C_shard, N_local, P, M, levels, workspace, ws_bytes, nullptr, stream);
+  // the caller's stream continues after every communication op of the product
+  if ((e = cudaEventRecord(ds.end_ev, cs)) == cudaSuccess) e = cudaStreamWaitEvent(st, ds.end_ev, 0);
+  return cuda_status(e);
 }
 
 int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, void* stream) {

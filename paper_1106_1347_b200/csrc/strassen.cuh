@@ -21,7 +21,10 @@
 //    (c4, d = 3: 24.6 -> 22.4 ms per product).
 // All add/sub kernels are HBM-bound grid-stride loops with 16-byte vectors where aligned.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
+#include "gemm_comb.cuh"
 #include "gemm_tma.cuh"
 
 namespace mmk {
@@ -37,6 +40,9 @@ struct FormArgs {
   double* dst;            // child level: 7 cnt dense nodes of h_rows x h_cols
   int64_t h_rows, h_cols; // child (= quadrant) dims
   int64_t cnt;
+  int64_t u0, u1;         // row units [u0, u1) of the cnt * h_rows this pass covers (all by default;
+                          // a sub-range forms the operands from the rows of B that have already
+                          // arrived -- the multi-GPU broadcast overlap, mm_dist_step MM_OP_FORM_B)
 };
 
 // ---- vector I/O: V = 4 -> 256-bit LDG/STG (sm_100a), V = 2 -> 128-bit, V = 1 -> scalar
@@ -81,7 +87,8 @@ __device__ __forceinline__ void ld_quad(const FormArgs& a, const double* base, i
 // Work mapping of the add/sub kernels: a "row unit" is one row of one node's quadrant; 2^TPRS
 // threads sweep a row unit with V-wide vectors (consecutive threads -> consecutive vectors,
 // so every warp access is a contiguous, fully used run of sectors), 256 >> TPRS row units per
-// block, grid-stride over all cnt * h_rows units.  Index arithmetic is once per row unit.
+// block, grid-stride over the pass's units [u0, u1) (all cnt * h_rows of them unless a multi-GPU
+// panel restricts the first B-side pass).  Index arithmetic is once per row unit.
 
 // the seven child operands of one node at one element position, from its four quadrants'
 // values: P:271-277 (StrassenNaiv) / P:300-306 (StrassenWinograd), the oracle's operations in
@@ -151,9 +158,8 @@ template <int VARIANT, int SIDE, int V>
 __global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a, int tprs) {
   const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
   const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
-  const int64_t units = a.cnt * a.h_rows;
   const int64_t child_elems = a.h_rows * a.h_cols;
-  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+  for (int64_t u = a.u0 + int64_t(blockIdx.x) * rpb + sub; u < a.u1; u += int64_t(gridDim.x) * rpb) {
     const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
     const double* base = a.src + q * a.src_stride;
     double* d0 = a.dst + (7 * q) * child_elems + i * a.h_cols;
@@ -188,9 +194,8 @@ template <int VARIANT, int SIDE, int V>
 __global__ void __launch_bounds__(256) strassen_form2_kernel(FormArgs a, int tprs) {
   const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
   const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
-  const int64_t units = a.cnt * a.h_rows;
   const int64_t gelems = a.h_rows * a.h_cols;
-  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+  for (int64_t u = a.u0 + int64_t(blockIdx.x) * rpb + sub; u < a.u1; u += int64_t(gridDim.x) * rpb) {
     const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
     const double* base = a.src + q * a.src_stride;
     double* d0 = a.dst + (49 * q) * gelems + i * a.h_cols;
@@ -236,26 +241,40 @@ __global__ void __launch_bounds__(256) strassen_form2_kernel(FormArgs a, int tpr
 // grandchild g its 4 quadrant values, then the 7 great-grandchildren -- again exactly the
 // single-level operations in their order.  h_rows / h_cols: the great-grandchild dims (an
 // eighth of the parent's); dst holds 343 cnt nodes.  At d = 3 this is the whole formation.
+// The 64 inputs are staged in a THREAD-PRIVATE slice of shared memory (slot k of thread t at
+// k * F3_THREADS + t: conflict-free, no barrier -- no thread reads another's values) instead of
+// registers: a child's sub-block value needs only 4 of them, so a thread keeps 16 child values
+// live instead of 64 inputs (255 registers with spills and one 256-thread block per SM before;
+// ~100 registers and three 128-thread blocks per SM now).
+constexpr int F3_THREADS = 128;
+constexpr size_t F3_SMEM = size_t(64) * F3_THREADS * sizeof(double);  // 64 KB
+
 template <int VARIANT, int SIDE>
-__global__ void __launch_bounds__(256) strassen_form3_kernel(FormArgs a, int tprs) {
+__global__ void __launch_bounds__(F3_THREADS) strassen_form3_kernel(FormArgs a, int tprs) {
+  extern __shared__ double f3_x[];
+  double* xs = f3_x + threadIdx.x;  // this thread's 64 slots, stride F3_THREADS
   const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
-  const int64_t rpb = 256 >> tprs, step = int64_t(1) << tprs;
-  const int64_t units = a.cnt * a.h_rows;
+  const int64_t rpb = F3_THREADS >> tprs, step = int64_t(1) << tprs;
   const int64_t gelems = a.h_rows * a.h_cols;
-  for (int64_t u = int64_t(blockIdx.x) * rpb + sub; u < units; u += int64_t(gridDim.x) * rpb) {
+  for (int64_t u = a.u0 + int64_t(blockIdx.x) * rpb + sub; u < a.u1; u += int64_t(gridDim.x) * rpb) {
     const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
     const double* base = a.src + q * a.src_stride;
     double* d0 = a.dst + (343 * q) * gelems + i * a.h_cols;
     for (int64_t j = lt; j < a.h_cols; j += step) {
-      double x[8][8];
+#pragma unroll 1
+      for (int pr0 = 0; pr0 < 8; pr0 += 2) {  // 16 loads in flight per thread, then parked
+        double v[16];
 #pragma unroll
-      for (int pr = 0; pr < 8; ++pr)
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-        for (int pc = 0; pc < 8; ++pc) {
-          double v[1];
-          ld_quad<1>(a, base, i + pr * a.h_rows, j + pc * a.h_cols, v);
-          x[pr][pc] = v[0];
-        }
+          for (int pc = 0; pc < 8; ++pc)
+            ld_quad<1>(a, base, i + (pr0 + r) * a.h_rows, j + pc * a.h_cols, &v[r * 8 + pc]);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) xs[(pr0 * 8 + k) * F3_THREADS] = v[k];
+      }
+      // volatile: read from shared memory where used, not hoisted back into 64 registers
+      const volatile double* xv = xs;
+      auto x = [&](int pr, int pc) { return xv[(pr * 8 + pc) * F3_THREADS]; };
       double* p = d0 + j;
 #pragma unroll 1
       for (int c = 0; c < 7; ++c) {
@@ -264,7 +283,7 @@ __global__ void __launch_bounds__(256) strassen_form3_kernel(FormArgs a, int tpr
         for (int ra = 0; ra < 4; ++ra)
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb)
-            ch[ra][cb] = form1<VARIANT, SIDE>(c, x[ra][cb], x[ra][4 + cb], x[4 + ra][cb], x[4 + ra][4 + cb]);
+            ch[ra][cb] = form1<VARIANT, SIDE>(c, x(ra, cb), x(ra, 4 + cb), x(4 + ra, cb), x(4 + ra, 4 + cb));
 #pragma unroll 1
         for (int g = 0; g < 7; ++g) {
           double gq[2][2];
@@ -552,7 +571,7 @@ inline unsigned grid_for(int64_t units, int tprs, int sms) {
 
 template <int VARIANT, int SIDE>
 cudaError_t launch_form_side(const FormArgs& fa, int v, int sms, cudaStream_t st) {
-  const int64_t units = fa.cnt * fa.h_rows;
+  const int64_t units = fa.u1 - fa.u0;
   const int tprs = tpr_shift(fa.h_cols, v);
   if (v == 4) {
     constexpr auto k = strassen_form_kernel<VARIANT, SIDE, 4>;
@@ -576,7 +595,7 @@ cudaError_t launch_form_level(int side, const FormArgs& fa, int v, int sms, cuda
 template <int VARIANT, int SIDE>
 cudaError_t launch_form2_side(const FormArgs& fa, int v, int sms, cudaStream_t st) {
   if (v > 2) v = 2;  // 16 inputs x V live per thread: V = 4 would spill (V = 1: same time)
-  const int64_t units = fa.cnt * fa.h_rows;
+  const int64_t units = fa.u1 - fa.u0;
   const int tprs = tpr_shift(fa.h_cols, v);
   if (v == 2) {
     constexpr auto k = strassen_form2_kernel<VARIANT, SIDE, 2>;
@@ -591,10 +610,23 @@ cudaError_t launch_form2_side(const FormArgs& fa, int v, int sms, cudaStream_t s
 
 template <int VARIANT, int SIDE>
 cudaError_t launch_form3_side(const FormArgs& fa, int sms, cudaStream_t st) {
-  const int64_t units = fa.cnt * fa.h_rows;
-  const int tprs = tpr_shift(fa.h_cols, 1);
   constexpr auto k = strassen_form3_kernel<VARIANT, SIDE>;
-  k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, tprs);
+  cudaError_t e = smem_attr_once<k>(F3_SMEM);
+  if (e != cudaSuccess) return e;
+  static int per_sm = 0;  // resident blocks per SM (shared memory bound: 3 x 64 KB)
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, F3_THREADS, F3_SMEM) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 2;
+    }
+  }
+  const int64_t units = fa.u1 - fa.u0;
+  int tprs = tpr_shift(fa.h_cols, 1);
+  if (tprs > 7) tprs = 7;  // at most one row unit per 128-thread block
+  int64_t b = cdiv(units, int64_t(F3_THREADS >> tprs));
+  const int64_t cap = int64_t(sms) * per_sm;
+  if (b > cap) b = cap;
+  k<<<unsigned(b < 1 ? 1 : b), F3_THREADS, F3_SMEM, st>>>(fa, tprs);
   note_launch();
   return cudaGetLastError();
 }
@@ -643,11 +675,25 @@ cudaError_t launch_combine2_level(const CombineArgs& ca, int v, int sms, cudaStr
   return cudaGetLastError();
 }
 
+// Phases of one product (mm_dist_step runs them separately so the first B-side formation pass
+// can follow the broadcast of B panel by panel; mm_strassen runs SP_ALL):
+enum { SP_FORM_A = 1, SP_FORM_B_FIRST = 2, SP_FORM_B_REST = 4, SP_LEAF_COMBINE = 8, SP_ALL = 15 };
+
+// Span (levels) of the first formation pass at depth d >= 1, and its row units: the first pass on
+// the B side reads B rows {u + r * (Pp >> span) : r < 2^span} for unit u in [0, Pp >> span).
+inline int first_form_span(int d) {
+  int steps[16][2];
+  form_schedule(d, steps);
+  return steps[0][1] - steps[0][0];
+}
+
 template <int VARIANT>
 cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
-                         const StrassenPlan& pl, char* ws, int sms, cudaStream_t st) {
+                         const StrassenPlan& pl, char* ws, int sms, cudaStream_t st, int phases = SP_ALL,
+                         int64_t b_u0 = 0, int64_t b_u1 = INT64_MAX) {
   const int d = pl.depth;
   if (d == 0) {
+    if (!(phases & SP_LEAF_COMBINE)) return cudaSuccess;
     GemmProblem pr{A, B, C, N, P, M, P, M, M, 0, 0, 0, 1};
     return launch_dgemm(pr, st, sms);
   }
@@ -656,18 +702,21 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
   double* T[2] = {reinterpret_cast<double*>(ws + pl.offT[0]), reinterpret_cast<double*>(ws + pl.offT[1])};
   double* Hb = reinterpret_cast<double*>(ws + pl.offH);
   double* Cb[2] = {reinterpret_cast<double*>(ws + pl.offC[0]), reinterpret_cast<double*>(ws + pl.offC[1])};
-  // Formation schedule: an odd remaining depth >= 3 starts with a three-level pass
-  // (strassen_form3_kernel), then two levels per pass (strassen_form2_kernel), a single level
-  // only when d = 1, so the deepest -- largest -- intermediate levels are never written.  The produced levels alternate between the two buffers, the last (level d, read
-  // by the leaf GEMM) in buffer 0; buffer 1 is sized for level d - 1 >= any earlier level.
-  // Combination level l >= 1 lives in Cb[(d - 1 - l) % 2].
+  // Formation schedule (form_schedule): an odd remaining depth >= 3 starts with a three-level pass
+  // (strassen_form3_kernel), then two levels per pass (strassen_form2_kernel), a single level only
+  // when d = 1, so the deepest -- largest -- intermediate levels are never written.  Pass k writes
+  // buffer (ns - 1 - k) % 2 (the last pass, level d read by the leaf GEMM, writes buffer 0) and
+  // reads what pass k - 1 wrote; make_strassen_plan sizes each buffer for the levels written to it.
   int steps[16][2];
   const int ns = form_schedule(d, steps);
   for (int side = 0; side < 2; ++side) {
+    const int want = side == 0 ? SP_FORM_A : (SP_FORM_B_FIRST | SP_FORM_B_REST);
+    if (!(phases & want)) continue;
     NvtxRange nvtx(side == 0 ? "strassen form (A side)" : "strassen form (B side)");
     const int64_t R = side == 0 ? pl.Np : pl.Pp, Ccols = side == 0 ? pl.Pp : pl.Mp;
     double** buf = side == 0 ? S : T;
     for (int k = 0; k < ns; ++k) {
+      if (side == 1 && !(phases & (k == 0 ? SP_FORM_B_FIRST : SP_FORM_B_REST))) continue;
       const int l = steps[k][0], span = steps[k][1] - l, two = span == 2;
       FormArgs fa;
       const int64_t r_l = R >> l, c_l = Ccols >> l;
@@ -688,6 +737,13 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
       fa.h_rows = r_l >> span;
       fa.h_cols = c_l >> span;
       fa.cnt = ipow7(l);
+      fa.u0 = 0;
+      fa.u1 = fa.cnt * fa.h_rows;
+      if (side == 1 && k == 0) {  // the B rows of this unit range are the ones that have arrived
+        fa.u0 = b_u0 < fa.u1 ? b_u0 : fa.u1;
+        fa.u1 = b_u1 < fa.u1 ? b_u1 : fa.u1;
+        if (fa.u0 >= fa.u1) continue;
+      }
       const int v = pick_vec(fa.src, fa.dst, fa.src_pitch, fa.src_stride, fa.h_cols);
       e = span == 3 ? launch_form3_level<VARIANT>(side, fa, sms, st)
           : two     ? launch_form2_level<VARIANT>(side, fa, v, sms, st)
@@ -695,22 +751,52 @@ cudaError_t run_strassen(const double* A, const double* B, double* C, int64_t N,
       if (e != cudaSuccess) return e;
     }
   }
-  // the 7^d leaf products, one batched DMMA launch
+  if (!(phases & SP_LEAF_COMBINE)) return cudaSuccess;
+  // the 7^d leaf products, one batched DMMA launch -- for Strassen-Winograd at depth >= 3 with
+  // the deepest combination fused into its epilogue (NEXT-1, gemm_comb.cuh: level d - 1 written
+  // straight into Hb, or into C at d = 1).  Measured at 8192^3 (profiles/r02/next1_comb.log):
+  // d = 3 22.38 -> 22.17 ms; d = 2 24.28 -> 24.65 ms (the seven children of a parent then span
+  // 7 x 64 MB of operands, more than L2 holds), hence the depth rule; it also needs >= 4 waves of
+  // CTAs (a CTA computes seven products).  MM_STRASSEN_FUSED_COMBINE=0 / 1 forces it off / on.
+  int dc = d;  // the level the combination passes start from
   {
     NvtxRange nvtx("strassen leaf products");
     const int64_t n = pl.Np >> d, p = pl.Pp >> d, m = pl.Mp >> d;
     GemmProblem pr{S[0], T[0], Hb, n, p, m, p, m, m, n * p, p * m, n * m, ipow7(d)};
-    e = launch_dgemm(pr, st, sms);
-    if (e != cudaSuccess) return e;
+    static const int force = [] {
+      const char* v = std::getenv("MM_STRASSEN_FUSED_COMBINE");
+      return v ? (v[0] == '1' ? 1 : 0) : -1;
+    }();
+    const int64_t ctas = cdiv(n, int64_t(GemmComb::BM)) * cdiv(m, int64_t(GemmComb::BN)) * ipow7(d - 1);
+    const bool fuse = force == 1 || (force == -1 && d >= 3 && ctas >= 4 * 3 * int64_t(sms));
+    e = cudaErrorNotSupported;
+    if (VARIANT == SV_WINOGRAD && fuse) {
+      CombStore o;
+      if (d == 1) {
+        o = CombStore{C, M, 0, N, M};
+      } else {
+        const int64_t rl = pl.Np >> (d - 1), cl = pl.Mp >> (d - 1);
+        o = CombStore{Hb, cl, rl * cl, rl, cl};
+      }
+      e = launch_dgemm_comb(pr, o, st);
+      if (e == cudaSuccess) dc = d - 1;
+      else if (e == cudaErrorNotSupported) cudaGetLastError();
+      else return e;
+    }
+    if (dc == d) {
+      e = launch_dgemm(pr, st, sms);
+      if (e != cudaSuccess) return e;
+    }
   }
   NvtxRange nvtx_combine("strassen combination");
-  // Combination schedule: two levels per pass from the deepest (largest) level down, a single
-  // level last when one remains; the k-th produced intermediate level lives in Cb[k % 2]
-  // (Cb[0] is sized for level d - 1, Cb[1] for d - 2 >= every later one).
+  // Combination schedule (combine_schedule): two levels per pass from the deepest (largest) level
+  // down, a single level last when one remains; the j-th intermediate level produced (> 0) is
+  // written to Cb[j % 2] and read by the next pass.  At d = 3 the passes are 3 -> 1 (into Cb[0])
+  // and 1 -> 0 (into C), so Cb[1] is never used and make_strassen_plan gives it no bytes.
   const double* Hsrc = Hb;
   int produced = 0;
   int csteps[16][2];
-  const int ncs = combine_schedule(d, csteps);
+  const int ncs = combine_schedule(dc, csteps);
   for (int k = 0; k < ncs; ++k) {
     const int l_from = csteps[k][0], l = csteps[k][1];  // this pass reads level l_from, writes level l
     const bool two = l_from - l == 2;

@@ -2,34 +2,53 @@
 
 C = A B is split by rows: rank r owns rows [r*ceil(N/g), min(N, (r+1)*ceil(N/g))) of A and C
 (workload.shard_rows uses the same rule); B is broadcast from `root` every product -- the one
-real exchange step of the path.  WinogradScaled additionally needs
-the GLOBAL ||A||_inf: each rank's local norm is max-all-reduced (8 bytes), ||B||_inf is local
-because B is replicated, so lambda is identical on every rank and to the 1-GPU run.
+real exchange step of the path.
 
-Per-entry arithmetic of every kernel depends only on (row of A, column of B, P) -- there is
-no split-K and y_i / z_k are per row / column -- so the classical, Kahan, Winograd and scaled
-Winograd shards are bitwise equal to the corresponding rows of the 1-GPU product.  Strassen on
-a shard recurses on (N_local x P x M) and agrees within its tolerance only.
+The schedule of one product is NOT written here: it comes from the C library
+(``mm_dist_schedule``, include/mm.h), a list of communication ops (broadcasts of row ranges of B,
+the max-all-reduce of WinogradScaled's norms), compute ops and record/wait events, a function of
+(method, P, M, levels, panels) only.  ``dist_gemm`` executes that list over torch.distributed
+(NCCL on GPUs; gloo in the CPU tests) and ``NativeComm`` has the library execute the same list
+with its own NCCL communicator (``mm_dist_gemm``).  Compute ops run through ``mm_dist_step`` --
+or through an injected callable, which is how the CPU tests drive the schedule with two ranks and
+the oracle as the local arithmetic.
 
-Broadcast/compute overlap, NaivStandard, NaivKahan and WinogradOriginal
-(and their fused variants): with panels > 1, B is broadcast as `panels` consecutive row panels
-(contiguous in memory, even boundaries), all enqueued at once on NCCL's stream; the product is
-accumulated panel by panel (mm_naive_ex / mm_kahan_ex / mm_winograd_ex), each launch waiting (on
-the device, not the host) for its own panel only, so the transfer of panel i+1 overlaps the work on
-panel i.  Every entry's running state -- the fma chain (reading R2), Kahan's (sum, err), Winograd's
-pair sum -- continues from panel to panel in k order, so the result is bitwise the one-shot product
-at any panel count; Winograd's y and z are computed from the full operands before the last panel.
-
-The compute and norm callables are injectable so that the host-side logic (sharding, the
-broadcast, the max-reduction and lambda, the panel schedule) is testable with world_size 2 on
-CPU (gloo).
+Per-entry arithmetic of every kernel depends only on (row of A, column of B, P) -- there is no
+split-K and y_i / z_k are per row / column -- so the classical, Kahan, Winograd and scaled
+Winograd shards are bitwise equal to the corresponding rows of the 1-GPU product (WinogradScaled
+max-all-reduces {||A_r||, ||B|| of the root}, so lambda is the 1-GPU lambda).  Strassen on a
+shard recurses on (N_local x P x M) and agrees within its tolerance only.  Panels are listed in
+increasing k and every running state continues from panel to panel, so any panel count gives the
+one-broadcast result bit for bit.
 """
 from __future__ import annotations
 
-from typing import Callable, Optional
+import ctypes
+from typing import Callable, List, Optional
 
 import torch
 import torch.distributed as dist
+
+# op kinds and streams of include/mm.h
+OP_BCAST, OP_ALLREDUCE_NORMS, OP_RECORD, OP_WAIT = 1, 2, 3, 4
+OP_NORMS, OP_PANEL, OP_YZ, OP_SCALE_A, OP_SCALE_B = 5, 6, 7, 8, 9
+OP_FORM_A, OP_FORM_B, OP_FORM_B_REST, OP_LEAF_COMBINE, OP_FULL = 10, 11, 12, 13, 14
+STREAM_COMPUTE, STREAM_COMM = 0, 1
+OP_NAMES = {OP_BCAST: "bcast", OP_ALLREDUCE_NORMS: "allreduce_norms", OP_RECORD: "record", OP_WAIT: "wait",
+            OP_NORMS: "norms", OP_PANEL: "panel", OP_YZ: "yz", OP_SCALE_A: "scale_a", OP_SCALE_B: "scale_b",
+            OP_FORM_A: "form_a", OP_FORM_B: "form_b", OP_FORM_B_REST: "form_b_rest",
+            OP_LEAF_COMBINE: "leaf_combine", OP_FULL: "full"}
+EX_ACCUMULATE, EX_KEEP_STATE, EX_FUSED = 1, 2, 4
+
+
+class DistOp(ctypes.Structure):
+    """mm_dist_op of include/mm.h."""
+    _fields_ = [("op", ctypes.c_int32), ("stream", ctypes.c_int32), ("index", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("lo", ctypes.c_int64), ("hi", ctypes.c_int64)]
+
+    def __repr__(self):
+        return (f"{OP_NAMES.get(self.op, self.op)}(stream={self.stream}, index={self.index}, flags={self.flags}, "
+                f"[{self.lo}, {self.hi}))")
 
 
 def shard_rows(N: int, world: int, rank: int):
@@ -38,106 +57,115 @@ def shard_rows(N: int, world: int, rank: int):
     return lo, min(N, lo + per)
 
 
-def _default_compute(method: str, A, B, out, levels, norms):
+def schedule(method: str, P: int, M: int, levels: int = 2, panels: int = 1) -> List[DistOp]:
+    """The op list of one distributed product (mm_dist_schedule; host only, no GPU needed)."""
     import paper_1106_1347_b200 as mm
 
-    if method == "winograd_scaled":
-        return mm.winograd_scaled(A, B, out=out, norms=norms)
-    if method in ("strassen", "strassen_winograd"):
-        return getattr(mm, method)(A, B, out=out, levels=levels)
-    return getattr(mm, method)(A, B, out=out)
+    L = mm.lib()
+    cap = 16 + 12 * max(1, panels)
+    ops = (DistOp * cap)()
+    n = L.mm_dist_schedule(mm.METHODS[method], P, M, levels, panels, ops, cap)
+    mm._check(n if n < 0 else 0, "mm_dist_schedule")
+    return [ops[i] for i in range(n)]
 
 
-def _default_norm(X):
+def workspace_bytes(method: str, N_local: int, P: int, M: int, levels: int = 2) -> int:
     import paper_1106_1347_b200 as mm
 
-    return mm.norm_inf(X)
+    return int(mm.lib().mm_dist_workspace_size(mm.METHODS[method], N_local, P, M, levels))
 
 
-PANEL_METHODS = ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused")
-
-
-def _default_panel(method, A_panel, B_panel, out, first: bool, last: bool, ctx: dict):
-    """One k-panel step on the GPU.  ctx holds the full operands ("A", "B") and the carried state
-    (Kahan's err "E"; Winograd's "y", "z", computed from the full operands before the last panel)."""
+def gpu_step(op: DistOp, ctx: dict) -> None:
+    """Run one compute op of the schedule through mm_dist_step on the current stream."""
     import paper_1106_1347_b200 as mm
 
-    fused = method.endswith("_fused")
-    if method == "naive":
-        return mm.naive_panel(A_panel, B_panel, out, accumulate=not first)
-    if method.startswith("kahan"):
-        if "E" not in ctx:
-            ctx["E"] = torch.empty_like(out)
-        return mm.kahan_panel(A_panel, B_panel, out, ctx["E"], accumulate=not first, keep_state=not last,
-                              fused=fused)
-    y = z = None
-    if last:
-        A, B = ctx["A"], ctx["B"]
-        y = torch.empty(A.shape[0], dtype=torch.float64, device=A.device)
-        z = torch.empty(B.shape[1], dtype=torch.float64, device=B.device)
-        mm.winograd_yz(A, B, y, z, fused=fused)
-    return mm.winograd_panel(A_panel, B_panel, out, y, z, accumulate=not first, keep_state=not last, fused=fused)
+    A, B, C, ws = ctx["A"], ctx["B"], ctx["out"], ctx["ws"]
+    N, P = A.shape
+    M = B.shape[1]
+    with torch.cuda.device(B.device):
+        rc = mm.lib().mm_dist_step(mm.METHODS[ctx["method"]], ctypes.byref(op), A.data_ptr() if N else None,
+                                   B.data_ptr(), C.data_ptr() if N else None, N, P, M, ctx["levels"],
+                                   int(ctx["is_root"]), ws.data_ptr() if ws is not None else None,
+                                   ws.numel() if ws is not None else 0,
+                                   torch.cuda.current_stream(B.device).cuda_stream)
+    mm._check(rc, f"mm_dist_step({OP_NAMES.get(op.op, op.op)})")
 
 
-def panels_supported(method: str, P: int, M: int) -> bool:
-    """NaivStandard always; Kahan / Winograd need the TMA-fed panel kernels: P and M even."""
-    return method == "naive" or (method in PANEL_METHODS and P % 2 == 0 and M % 2 == 0)
+_WS = {}
 
 
-def panel_bounds(P: int, panels: int):
-    """Consecutive k-panels [k0, k1) covering 0..P, boundaries even (16-byte aligned views)."""
-    panels = max(1, min(panels, P))
-    cuts = sorted({min(P, 2 * ((P * i) // (2 * panels))) for i in range(1, panels)} - {0, P})
-    b = [0] + cuts + [P]
-    return list(zip(b[:-1], b[1:]))
-
-
-def _dist_panels(method, A_local, B, out, root, group, panels, panel_compute):
-    P, M = B.shape
-    bounds = panel_bounds(P, panels)
-    works = [dist.broadcast(B[k0:k1], src=root, group=group, async_op=True) for k0, k1 in bounds]
-    if out is None:
-        out = torch.empty((A_local.shape[0], M), dtype=B.dtype, device=B.device)
-    ctx = {"A": A_local, "B": B}
-    for i, (k0, k1) in enumerate(bounds):
-        works[i].wait()  # NCCL: the current stream waits for this panel only; gloo: the host waits
-        if A_local.shape[0] > 0:
-            panel_compute(method, A_local[:, k0:k1], B[k0:k1], out, i == 0, i == len(bounds) - 1, ctx)
-    return out
+def _workspace(method, N, P, M, levels, device):
+    nbytes = workspace_bytes(method, N, P, M, levels)
+    if nbytes == 0:
+        return None
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
 
 
 def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None,
-              root: int = 0, group=None, levels: int = 2, compute: Optional[Callable] = None,
-              norm: Optional[Callable] = None, panels: int = 1,
-              panel_compute: Optional[Callable] = None) -> torch.Tensor:
-    """C_local = A_local B on every rank.  B must be allocated (P x M) on every rank; its content
-    on `root` is broadcast (in place) before / during the product.  A rank with no rows still
-    takes part in the collectives and returns an empty (0 x M) result.  panels > 1 (NaivStandard;
-    NaivKahan / WinogradOriginal and the fused variants when P and M are even): panelised broadcast
-    overlapped with the accumulation (NEXT-4); panel_compute(method, A_panel, B_panel, out, first,
-    last, ctx) performs one panel step."""
-    compute = compute or _default_compute
-    norm = norm or _default_norm
-    if panels > 1 and panels_supported(method, B.shape[0], B.shape[1]):
-        return _dist_panels(method, A_local, B, out, root, group, panels, panel_compute or _default_panel)
-    dist.broadcast(B, src=root, group=group)
-    norms = None
-    if method == "winograd_scaled":
-        nA = norm(A_local) if A_local.shape[0] > 0 else torch.zeros(1, dtype=torch.float64, device=B.device)
-        dist.all_reduce(nA, op=dist.ReduceOp.MAX, group=group)  # ||A||_inf = max over row blocks
-        norms = torch.cat([nA.reshape(1), norm(B).reshape(1)])
-    if A_local.shape[0] == 0:
-        return torch.empty((0, B.shape[1]), dtype=B.dtype, device=B.device)
-    return compute(method, A_local, B, out, levels, norms)
+              root: int = 0, group=None, levels: int = 2, panels: int = 1,
+              step: Optional[Callable] = None, ctx: Optional[dict] = None) -> torch.Tensor:
+    """C_local = A_local B on every rank, executing mm_dist_schedule(method, P, M, levels, panels)
+    over torch.distributed.  B must be allocated (P x M) on every rank; its content on `root` is
+    broadcast (in place) during the product.  A rank with no rows still takes part in the
+    collectives and returns an empty (0 x M) result.
+
+    Communication ops are issued as async collectives in list order (a collective issued after a
+    compute op is ordered after it by torch -- NCCL's stream waits for the current stream at issue);
+    a compute-side WAIT waits for the works recorded on that event (NCCL: the current stream waits
+    on the device; gloo: the host waits).  step(op, ctx) runs a compute op (default: mm_dist_step on
+    the GPU); ctx holds method, A, B, out, levels, is_root, the norms tensor the all-reduce
+    reduces, and the workspace."""
+    N, P = A_local.shape
+    M = B.shape[1]
+    if B.shape[0] != P:
+        raise ValueError("inner dimensions differ")
+    rank = dist.get_rank(group)
+    if out is None:
+        out = torch.empty((N, M), dtype=B.dtype, device=B.device)
+    ctx = dict(ctx or {})
+    ctx.update(method=method, A=A_local, B=B, out=out, levels=levels, is_root=rank == root)
+    if step is None:
+        step = gpu_step
+        ctx["ws"] = _workspace(method, N, P, M, levels, B.device)
+        if method.startswith("winograd_scaled"):
+            ctx["norms"] = ctx["ws"][:16].view(torch.float64)  # the workspace's leading {||A||, ||B||}
+    ctx.setdefault("norms", torch.zeros(2, dtype=torch.float64, device=B.device))
+    pending, events = [], {}
+    for op in schedule(method, P, M, levels, panels):
+        if op.op == OP_BCAST:
+            pending.append(dist.broadcast(B[op.lo:op.hi], src=root, group=group, async_op=True))
+        elif op.op == OP_ALLREDUCE_NORMS:
+            pending.append(dist.all_reduce(ctx["norms"], op=dist.ReduceOp.MAX, group=group, async_op=True))
+        elif op.op == OP_RECORD:
+            if op.stream == STREAM_COMM:
+                events[op.index] = pending
+                pending = []
+            # a compute-side record needs nothing: torch orders later collectives after it
+        elif op.op == OP_WAIT:
+            if op.stream == STREAM_COMPUTE:
+                for w in events.pop(op.index, []):
+                    w.wait()
+        else:
+            step(op, ctx)
+    for w in pending:
+        w.wait()
+    for ws_ in events.values():
+        for w in ws_:
+            w.wait()
+    return out
 
 
 class NativeComm:
-    """The C ABI's own multi-GPU layer (mm_dist_*: NCCL driven from libmm_b200.so, broadcast of B
-    and the panelised overlap on the library's streams).  torch.distributed only bootstraps it:
-    rank 0's 128-byte NCCL id reaches the other ranks through broadcast_object_list."""
+    """The C ABI's own multi-GPU layer (mm_dist_*: NCCL driven from libmm_b200.so, the same schedule
+    on the library's streams).  torch.distributed only bootstraps it: rank 0's 128-byte NCCL id
+    reaches the other ranks through broadcast_object_list."""
 
     def __init__(self, group=None):
-        import ctypes
         import os
 
         import paper_1106_1347_b200 as mm
@@ -175,14 +203,13 @@ class NativeComm:
         if out is None:
             out = torch.empty((N, M), dtype=torch.float64, device=B.device)
         mid = mm.METHODS[method]
-        lv = levels if method in ("strassen", "strassen_winograd") else 0
-        nbytes = int(self.L.mm_dist_workspace_size(mid, N, P, M, lv))
+        nbytes = int(self.L.mm_dist_workspace_size(mid, N, P, M, levels))
         if nbytes and (self._ws is None or self._ws.numel() < nbytes):
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=B.device)
         ws_ptr = self._ws.data_ptr() if nbytes else None
         s = stream if stream is not None else torch.cuda.current_stream(B.device)
         mm._check(self.L.mm_dist_gemm(mid, A_local.data_ptr() if N else None, B.data_ptr(),
-                                      out.data_ptr() if N else None, N, P, M, root, lv, panels, ws_ptr, nbytes,
+                                      out.data_ptr() if N else None, N, P, M, root, levels, panels, ws_ptr, nbytes,
                                       s.cuda_stream), f"mm_dist_gemm({method})")
         return out
 

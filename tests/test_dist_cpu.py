@@ -1,7 +1,10 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the row-block driver paper_1106_1347_b200.dist:
-sharding, the B broadcast, the max-all-reduce of ||A||_inf and the resulting lambda.  The local
-compute is injected (the oracle), so this exercises exactly the host-side logic the GPU path
-uses, and checks the per-rank results are bitwise the rows of the 1-process product."""
+"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU schedule: the op list the C library
+builds (mm_dist_schedule -- the same list mm_dist_gemm executes with NCCL) executed by
+paper_1106_1347_b200.dist over gloo, with every compute op emulated by the oracle.  This covers
+sharding, the panelised broadcast of B, the max-all-reduce of {||A_r||, ||B||} and lambda, and the
+order of every compute op against the arrival of the B rows it reads (B is NaN on non-root ranks
+until its rows land), for every method, several panel counts and Strassen depths; the per-rank
+results must be bitwise the rows of the 1-process oracle product."""
 import os
 import socket
 
@@ -22,58 +25,109 @@ def _free_port():
     return p
 
 
-def _oracle_compute(method, A, B, out, levels, norms):
+FIRST_SPAN = {1: 1, 2: 2, 3: 3, 4: 2, 5: 3}  # levels of the first formation pass
+
+
+def _oracle_step(op, ctx):
+    """Emulates one compute op of the schedule with the oracle (the arithmetic the GPU kernels are
+    checked against bitwise elsewhere) and checks that every B row the op reads has arrived."""
     import oracle
+    from paper_1106_1347_b200 import dist as d
 
-    A_np, B_np = A.numpy(), B.numpy()
-    if method == "naive":
-        C = oracle.naive_fma(A_np, B_np)
-    elif method == "kahan":
-        C = oracle.naive_kahan(A_np, B_np)
-    elif method == "kahan_fused":
-        C = oracle.naive_kahan_fused(A_np, B_np)
-    elif method == "winograd":
-        C = oracle.winograd_original(A_np, B_np)
-    elif method == "winograd_fused":
-        C = oracle.winograd_fused(A_np, B_np)
-    elif method == "winograd_scaled":
-        lam = oracle.lam(float(norms[0]), float(norms[1]))
-        idx = [(i, j) for i in range(A_np.shape[0]) for j in range(B_np.shape[1])]
-        C = oracle.entries(oracle.M_WINOGRAD_SCALED, A_np, B_np, idx, lam).reshape(A_np.shape[0], B_np.shape[1])
-    else:
-        raise ValueError(method)
-    return torch.from_numpy(C)
+    m, levels = ctx["method"], ctx["levels"]
+    A, B, C = ctx["A"].numpy(), ctx["B"].numpy(), ctx["out"].numpy()
+    N, P = A.shape
+    M = B.shape[1]
+    Bt = ctx["B_true"]
+    fused = m.endswith("_fused")
+    ctx["trace"].append(op.op)
 
+    def arrived(lo, hi):
+        assert np.array_equal(B[lo:hi], Bt[lo:hi]), (repr(op), "reads B rows that have not arrived")
 
-def _oracle_panel(method, A_panel, B_panel, out, first, last, ctx):
-    """The panel step of each method through the oracle's resumable loops (state kept in `out`
-    and ctx); the last Winograd panel applies the epilogue with y, z of the full operands."""
-    import oracle
-
-    C = out.numpy()
-    fused = method.endswith("_fused")
-    Ap, Bp = A_panel.numpy(), B_panel.numpy()
-    if first:
-        C[...] = 0.0
-    if method == "naive":
-        oracle.naive_fma_acc(Ap, Bp, C)
-    elif method.startswith("kahan"):
+    if op.op == d.OP_NORMS:
+        ctx["norms"][0] = oracle.norm_inf(A) if N else 0.0
+        ctx["norms"][1] = oracle.norm_inf(B) if ctx["is_root"] else 0.0
+        return
+    if N == 0:
+        return
+    lam = oracle.lam(float(ctx["norms"][0]), float(ctx["norms"][1])) if m.startswith("winograd_scaled") else 0
+    if op.op == d.OP_PANEL:
+        arrived(op.lo, op.hi)
+        first, last = not op.flags & d.EX_ACCUMULATE, not op.flags & d.EX_KEEP_STATE
+        assert bool(op.flags & d.EX_FUSED) == fused
         if first:
-            ctx["E"] = np.zeros_like(C)
-        oracle.naive_kahan_acc(Ap, Bp, C, ctx["E"], fused)
+            C[...] = 0.0
+        k0, k1 = op.lo, op.hi
+        if m == "naive":
+            oracle.naive_fma_acc(A[:, k0:k1], B[k0:k1], C)
+        elif m.startswith("kahan"):
+            if first:
+                ctx["E"] = np.zeros_like(C)
+            oracle.naive_kahan_acc(A[:, k0:k1], B[k0:k1], C, ctx["E"], fused)
+        elif m.startswith("winograd_scaled"):
+            oracle.winograd_pairs_acc(ctx["As"][:, k0:k1], ctx["Bs"][k0:k1], C, fused)
+            if last:
+                arrived(0, P)
+                yz = oracle.winograd_yz_fused if fused else oracle.winograd_yz
+                C[...] = oracle.winograd_finish(C, *yz(ctx["As"], ctx["Bs"]))
+        else:
+            oracle.winograd_pairs_acc(A[:, k0:k1], B[k0:k1], C, fused)
+            if last:
+                C[...] = oracle.winograd_finish(C, *ctx["yz"])
+    elif op.op == d.OP_YZ:
+        arrived(0, P)
+        ctx["yz"] = (oracle.winograd_yz_fused if fused else oracle.winograd_yz)(A, B)
+    elif op.op == d.OP_SCALE_A:
+        ctx["As"] = oracle.scalar_mul(2.0 ** lam, A)
+        ctx["Bs"] = np.full((P, M), np.nan)
+    elif op.op == d.OP_SCALE_B:
+        arrived(op.lo, op.hi)
+        ctx["Bs"][op.lo:op.hi] = oracle.scalar_mul(2.0 ** -lam, B[op.lo:op.hi])
+    elif op.op in (d.OP_FORM_A, d.OP_FORM_B, d.OP_FORM_B_REST):
+        span, h = _first_pass_units(P, levels)
+        if op.op == d.OP_FORM_B:  # quadrant rows [lo, hi) read B rows u + r h, r < 2^span
+            for r in range(1 << span):
+                arrived(min(P, r * h + op.lo), min(P, r * h + op.hi))
+            ctx.setdefault("formed", set()).update(range(op.lo, op.hi))
+        elif op.op == d.OP_FORM_B_REST:
+            assert ctx.get("formed") == set(range(h)), "B-side formation of every unit before the rest"
+    elif op.op == d.OP_LEAF_COMBINE:
+        arrived(0, P)
+        assert ctx.get("formed", set(range(_first_pass_units(P, levels)[1]))) == set(
+            range(_first_pass_units(P, levels)[1]))
+        C[...] = _oracle_full(m, A, B, levels, lam)
+    elif op.op == d.OP_FULL:
+        arrived(0, P)
+        C[...] = _oracle_full(m, A, B, levels, lam)
     else:
-        oracle.winograd_pairs_acc(Ap, Bp, C, fused)
-        if last:
-            A, B = ctx["A"].numpy(), ctx["B"].numpy()
-            y, z = oracle.winograd_yz_fused(A, B) if fused else oracle.winograd_yz(A, B)
-            C[...] = oracle.winograd_finish(C, y, z)
-    return out
+        raise AssertionError(f"unexpected compute op {op!r}")
 
 
-def _oracle_norm(X):
+def _first_pass_units(P, levels):
+    # reading R10: P padded to a multiple of 2^(levels+1); the first pass spans FIRST_SPAN levels
+    q = 2 << levels
+    span = FIRST_SPAN[levels]
+    return span, (-(-P // q) * q) >> span
+
+
+def _oracle_full(m, A, B, levels, lam):
     import oracle
 
-    return torch.tensor([oracle.norm_inf(X.numpy())], dtype=torch.float64)
+    N, P, M = A.shape[0], A.shape[1], B.shape[1]
+    if m in ("strassen", "strassen_winograd"):
+        lv, pad = oracle.plan(N, P, M, levels)
+        return oracle.strassen(0 if m == "strassen" else 1, A, B, levels=lv, pad=pad, base=oracle.BASE_FMA)
+    if m.startswith("winograd_scaled"):
+        code = oracle.M_WINOGRAD_SCALED_FUSED if m.endswith("_fused") else oracle.M_WINOGRAD_SCALED
+        idx = [(i, j) for i in range(N) for j in range(M)]
+        return oracle.entries(code, A, B, idx, lam).reshape(N, M)
+    return {"naive": oracle.naive_fma, "kahan": oracle.naive_kahan, "kahan_fused": oracle.naive_kahan_fused,
+            "winograd": oracle.winograd_original, "winograd_fused": oracle.winograd_fused}[m](A, B)
+
+
+METHODS = ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused", "winograd_scaled",
+           "winograd_scaled_fused", "strassen", "strassen_winograd")
 
 
 def _worker(rank, world, port, N, P, M, seed, q):
@@ -92,35 +146,53 @@ def _worker(rank, world, port, N, P, M, seed, q):
         lo, hi = shard_rows(N, world, rank)
         assert (lo, hi) == workload.shard_rows(N, world, rank)
         A_loc = torch.from_numpy(np.ascontiguousarray(A[lo:hi]))
-        Bt = torch.from_numpy(B.copy()) if rank == 0 else torch.zeros((P, M), dtype=torch.float64)
-        out = {}
-        for m in ("naive", "kahan", "winograd", "winograd_scaled"):
-            C = dist_gemm(m, A_loc, Bt, compute=_oracle_compute, norm=_oracle_norm)
-            out[m] = C.numpy().copy()
-        assert np.array_equal(Bt.numpy(), B)  # broadcast delivered B everywhere
-        # NEXT-4: panelised broadcast + state-continuing accumulation, B re-broadcast from scratch
-        # (Kahan / Winograd take the panel path only for even P and M, else the one-shot compute)
-        for panels in (2, 3, 5):
-            for m in ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused"):
-                Bp = torch.from_numpy(B.copy()) if rank == 0 else torch.full((P, M), np.nan, dtype=torch.float64)
-                C = dist_gemm(m, A_loc, Bp, panels=panels, panel_compute=_oracle_panel, compute=_oracle_compute)
-                assert np.array_equal(Bp.numpy(), B)
-                out[f"{m}_p{panels}"] = C.numpy().copy()
-        q.put((rank, lo, hi, out))
+        out, traces = {}, {}
+        for panels in (1, 2, 3, 5):
+            for m in METHODS:
+                for levels in ((1, 2, 3) if m.startswith("strassen") else (2,)):
+                    # B re-broadcast from scratch: NaN everywhere but on the root
+                    Bp = torch.from_numpy(B.copy()) if rank == 0 else torch.full((P, M), np.nan, dtype=torch.float64)
+                    ctx = {"B_true": B, "trace": []}
+                    C = dist_gemm(m, A_loc, Bp, panels=panels, levels=levels, step=_oracle_step, ctx=ctx)
+                    assert np.array_equal(Bp.numpy(), B)  # the broadcast delivered all of B
+                    out[(m, panels, levels)] = C.numpy().copy()
+                    traces[(m, panels, levels)] = ctx["trace"]
+        q.put((rank, lo, hi, out, traces))
+    except BaseException as e:  # report instead of leaving the parent waiting on the queue
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc(), None, None))
+        raise e
     finally:
         dist.destroy_process_group()
 
 
-def test_panel_bounds():
-    from paper_1106_1347_b200.dist import panel_bounds
+def test_schedule_panel_bounds():
+    # the k-panels of the C schedule: consecutive, even boundaries, at most `panels` of them
+    from paper_1106_1347_b200 import dist as d
 
-    for P in (1, 2, 7, 16, 1001, 8192):
-        for n in (1, 2, 3, 8, 64):
-            b = panel_bounds(P, n)
+    for P in (2, 16, 1000, 8192):
+        for n in (2, 3, 8, 64):
+            b = [(o.lo, o.hi) for o in d.schedule("naive", P, 64, 2, n) if o.op == d.OP_PANEL]
             assert b[0][0] == 0 and b[-1][1] == P
             assert all(k0 < k1 for k0, k1 in b) and all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
             assert all(k0 % 2 == 0 for k0, _ in b)
             assert len(b) <= n
+
+
+def test_schedule_covers_b_once():
+    # every row of B is broadcast exactly once, whatever the method, levels and panel count
+    from paper_1106_1347_b200 import dist as d
+
+    for m in METHODS:
+        for P, M in ((8192, 8192), (1001, 3000), (20, 10), (13, 7)):
+            for lv in (-1, 0, 1, 2, 3, 4, 5):
+                for n in (1, 2, 5, 64):
+                    rows = np.zeros(P, dtype=np.int64)
+                    for o in d.schedule(m, P, M, lv, n):
+                        if o.op == d.OP_BCAST:
+                            rows[o.lo:o.hi] += 1
+                    assert (rows == 1).all(), (m, P, M, lv, n)
 
 
 def _run(world, N, P, M, seed):
@@ -130,14 +202,23 @@ def _run(world, N, P, M, seed):
     procs = [ctx.Process(target=_worker, args=(r, world, port, N, P, M, seed, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=240) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = []
+    try:
+        for _ in procs:
+            r = q.get(timeout=240)
+            assert r[1] != "error", r[2]
+            res.append(r)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:  # a rank left waiting in a collective by a failed peer
+            if p.is_alive():
+                p.kill()
     return sorted(res, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16), (7, 20, 10)])
+@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16), (7, 20, 10), (12, 32, 6)])
 def test_row_sharded_bitwise(shape):
     import oracle
     import workload
@@ -146,17 +227,25 @@ def test_row_sharded_bitwise(shape):
     res = _run(2, N, P, M, seed=N + P + M)
     A, B = workload.custom(N, P, M, seed=N + P + M)
     A = A * 1e5
-    full = {
-        "naive": oracle.naive_fma(A, B),
-        "kahan": oracle.naive_kahan(A, B),
-        "kahan_fused": oracle.naive_kahan_fused(A, B),
-        "winograd": oracle.winograd_original(A, B),
-        "winograd_fused": oracle.winograd_fused(A, B),
-        "winograd_scaled": oracle.winograd_scaled(A, B)[0],
-    }
-    assert oracle.winograd_scaled(A, B)[1] != 0
-    for rank, lo, hi, out in res:
-        for m, C in out.items():
-            assert C.shape == (hi - lo, M)
-            assert np.array_equal(C, full[m.split("_p")[0]][lo:hi]), (rank, m)
-    assert sum(hi - lo for _, lo, hi, _ in res) == N
+    full = {m: _oracle_full(m, A, B, 0, 0) for m in METHODS if not m.startswith(("winograd_scaled", "strassen"))}
+    C, lam = oracle.winograd_scaled(A, B)
+    assert lam != 0
+    full["winograd_scaled"] = C
+    full["winograd_scaled_fused"] = oracle.winograd_scaled_fused(A, B)[0]
+    for rank, lo, hi, out, traces in res:
+        for (m, panels, levels), Cr in out.items():
+            assert Cr.shape == (hi - lo, M)
+            if hi == lo:
+                continue
+            if m.startswith("strassen"):  # recursion on the shard: the oracle on the same shard
+                assert np.array_equal(Cr, _oracle_full(m, A[lo:hi], B, levels, 0)), (rank, m, panels, levels)
+            else:
+                assert np.array_equal(Cr, full[m][lo:hi]), (rank, m, panels)
+    assert sum(hi - lo for _, lo, hi, _, _ in res) == N
+    # the panel paths really ran where the schedule allows them
+    _, _, _, _, traces = res[0]
+    from paper_1106_1347_b200 import dist as d
+
+    assert d.OP_PANEL in traces[("naive", 3, 2)]
+    assert (d.OP_PANEL in traces[("winograd_scaled", 3, 2)]) == (P % 2 == 0 and M % 2 == 0)
+    assert d.OP_FORM_B in traces[("strassen_winograd", 2, 2)]

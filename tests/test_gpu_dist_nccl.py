@@ -29,7 +29,7 @@ SCRIPT = textwrap.dedent(r"""
     dA = torch.from_numpy(A * 1e3).to(dev)
     hB = torch.from_numpy(B).to(dev)
     for m in ("naive", "kahan", "winograd", "winograd_scaled", "strassen", "strassen_winograd", "kahan_fused",
-              "winograd_fused"):
+              "winograd_fused", "winograd_scaled_fused"):
         kw = {"levels": 2} if m.startswith("strassen") else {}
         ref = getattr(mm, m)(dA, hB, **kw)
         for panels in (1, 4, 7):
@@ -40,7 +40,7 @@ SCRIPT = textwrap.dedent(r"""
     # odd P: Kahan / Winograd fall back to one broadcast + the one-shot kernel (cp.async paths)
     A3, B3 = workload.custom(300, 1001, 260, seed=4)
     dA3, hB3 = torch.from_numpy(A3).to(dev), torch.from_numpy(B3).to(dev)
-    for m in ("naive", "kahan", "winograd"):
+    for m in ("naive", "kahan", "winograd", "winograd_scaled"):
         ref = getattr(mm, m)(dA3, hB3)
         C = dist_gemm(m, dA3, hB3.clone(), panels=4)
         torch.cuda.synchronize()
