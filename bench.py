@@ -402,12 +402,13 @@ def run_mine(args):
             Cm = outs[m][ii][:, jj].cpu().numpy()
             res[m]["rel_err_vs_exact"] = float(np.abs(Cm - X).sum(axis=1).max()) / (nA * nB) if nA * nB > 0 else 0.0
         err_note = (f"rows {rows} of rank 0's shard, {'all' if M <= 8192 else len(cols)} columns, "
-                    f"against the exactly rounded product (TwoProduct + fsum)")
+                    f"against the product to twice double precision (Dot2: TwoProduct + TwoSum)")
     else:
         err_note = None
 
     # roofline of the dominant kernel (largest share of the step)
-    traffic = load_traffic()
+    # (the DRAM bytes per launch were captured at c4's full size: reported for that workload only)
+    traffic = load_traffic() if (args.config == "c4" and world == 1) else {}
     n_eff = n_loc
     kernels = {
         "naive": ("tensor", 2.0 * n_eff * P * M, peaks["dmma_tflops"], "dgemm_tma_kernel"),

@@ -69,6 +69,12 @@ def schedule(method: str, P: int, M: int, levels: int = 2, panels: int = 1) -> L
     return [ops[i] for i in range(n)]
 
 
+def panel_bounds(P: int, panels: int):
+    """The k-panels [k0, k1) the schedule uses for P (those of NaivStandard's schedule)."""
+    b = [(o.lo, o.hi) for o in schedule("naive", P, 2, 0, panels) if o.op == OP_PANEL]
+    return b or [(0, P)]
+
+
 def workspace_bytes(method: str, N_local: int, P: int, M: int, levels: int = 2) -> int:
     import paper_1106_1347_b200 as mm
 

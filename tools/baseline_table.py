@@ -1,8 +1,9 @@
 """Render BASELINE.md section 4's per-configuration table from a `tools/table_bench.py` JSONL
-(device timings on one B200) and `profiles/r01/oracle_timing.jsonl` (the CPU oracle on the GPU
-box's host), and splice it into BASELINE.md in place of the current table.
+(device timings on one B200), an optional `tools/kernel_times.py` JSONL (kernel-only ncu times)
+and `profiles/r01/oracle_timing.jsonl` (the CPU oracle on the GPU box's host), and splice it into
+BASELINE.md in place of the current table.
 
-    python tools/baseline_table.py profiles/r01/table_v9.jsonl [--write]
+    python tools/baseline_table.py profiles/r02/table_r02.jsonl [--kernels profiles/r02/kernel_times.jsonl] [--write]
 """
 import json
 import os
@@ -10,9 +11,10 @@ import re
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = ("| cfg | method | levels | GPUs | t median (ms) | GFLOP/s (2NPM/t) | fraction of P64 | executed GFLOP/s "
-          "(Strassen) | ‖C−N‖∞ / (‖A‖∞‖B‖∞), N = NaivKahan | parity vs oracle | oracle t (1 core) | "
-          "oracle t (16 cores) |")
+HEADER = ("| cfg | method | levels | GPUs | t median (ms) | kernel-only t (ms, ncu) | GFLOP/s (2NPM/t) | fraction of P64 "
+          "| executed GFLOP/s (Strassen) | ‖C−N‖∞ / (‖A‖∞‖B‖∞), N = NaivKahan | ‖C−AB‖∞ / (‖A‖∞‖B‖∞), 2 rows | "
+          "parity vs oracle | oracle t (1 core) | oracle t (16 cores) |")
+NCOLS = 14
 ORACLE_NAME = {"naive": "naive_standard", "kahan": "naive_kahan", "winograd": "winograd_original",
                "winograd_scaled": "winograd_scaled", "strassen": "strassen_paper_plan",
                "strassen_winograd": "strassen_winograd_paper_plan"}
@@ -34,8 +36,18 @@ def oracle_times(path):
     return one, many
 
 
-def rows(table_path, oracle_path):
+def kernel_times(path):
+    out = {}
+    if path:
+        for line in open(path):
+            r = json.loads(line)
+            out[(r["config"], r["method"], r["levels"])] = r["kernel_ms"]
+    return out
+
+
+def rows(table_path, oracle_path, kernels_path=None):
     one, many = oracle_times(oracle_path)
+    kt = kernel_times(kernels_path)
     out = []
     for line in open(table_path):
         r = json.loads(line)
@@ -49,15 +61,20 @@ def rows(table_path, oracle_path):
         show_oracle = (not strassen) or lv == -1
         t1 = one.get(okey, "") if show_oracle else ""
         t16 = many.get(okey, "") if show_oracle else ""
-        out.append(f"| {r['config']} | {m} | {levels} | 1 | {r['ms']:.4g} | {r['gflops']:.0f} | "
-                   f"{r['frac_fp64_peak']:.3f} | {executed} | {r['rel_err_vs_kahan']:.2e} | {parity} | {t1} | {t16} |")
+        k = kt.get((r["config"], m, lv))
+        ks = f"{k:.4g}" if k is not None else ""
+        ex = f"{r['rel_err_vs_exact']:.2e}" if "rel_err_vs_exact" in r else ""
+        out.append(f"| {r['config']} | {m} | {levels} | 1 | {r['ms']:.4g} | {ks} | {r['gflops']:.0f} | "
+                   f"{r['frac_fp64_peak']:.3f} | {executed} | {r['rel_err_vs_kahan']:.2e} | {ex} | {parity} | {t1} | "
+                   f"{t16} |")
     return out
 
 
 def main(argv):
     table = argv[0]
-    body = rows(table, os.path.join(ROOT, "profiles", "r01", "oracle_timing.jsonl"))
-    text = "\n".join([HEADER, "|" + "---|" * 12] + body)
+    kernels = argv[argv.index("--kernels") + 1] if "--kernels" in argv else None
+    body = rows(table, os.path.join(ROOT, "profiles", "r01", "oracle_timing.jsonl"), kernels)
+    text = "\n".join([HEADER, "|" + "---|" * NCOLS] + body)
     if "--write" not in argv:
         print(text)
         return
@@ -67,7 +84,7 @@ def main(argv):
     end = s.find("\n\n", start)
     end = len(s) if end < 0 else end
     s = s[:start] + text + s[end:]
-    s = re.sub(r"profiles/r01/table_v\d+\.jsonl", "profiles/r01/" + os.path.basename(table), s)
+    s = re.sub(r"profiles/r0\d/table_\w+\.jsonl", os.path.relpath(table, ROOT), s)
     open(path, "w").write(s)
     print(f"BASELINE.md table regenerated from {table} ({len(body)} rows)")
 
