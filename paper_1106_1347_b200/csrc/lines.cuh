@@ -70,11 +70,14 @@ struct LineJob {
   int op;
   int scale_sel;                 // -1: unscaled; 0: x 2^lambda; 1: x 2^-lambda (lambda from norms)
   int bulk;                      // 1: tiles arrive by TMA (map[job]); 0: 8-byte cp.async fallback
+  int cbulk;                     // 1: the scaled copy leaves by TMA store (cmap[job]) from the tile,
+                                 //    scaled in place; 0: per-lane global stores
   int blocks;                    // 32-line blocks of this job
 };
 
 struct LineLaunch {
   CUtensorMap map[2];               // TMA maps of the jobs' operands (when bulk)
+  CUtensorMap cmap[2];              // TMA maps of the jobs' copies (when cbulk)
   LineJob job[2];
   int njobs;
   const unsigned long long* norms;  // {||A||, ||B||} bit patterns (for scale_sel >= 0)
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   }
   const LineJob& jb = L.job[ji];
   const int64_t l0 = int64_t(b) * LN_LINES;
-  const int64_t KT = cdiv(jb.len, LN_TK);
+  const int KT = int(cdiv(jb.len, LN_TK));
 
   double s = 1.0;
   if (SCALED && jb.scale_sel >= 0) {
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
 
   if (lane == 0) {
     if (jb.bulk) tma_prefetch_desc(&L.map[ji]);
+    if (jb.cbulk) tma_prefetch_desc(&L.cmap[ji]);
     for (int st = 0; st < S; ++st) mbar_init(bars + st, jb.bulk ? 1 : LN_LINES);
     fence_mbar_init();
   }
@@ -183,28 +187,35 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
 #pragma unroll 1
   for (int st = 0; st < S; ++st)
     if (st < KT) ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, st, lane);
+  // ring positions kept incrementally (S is a launch parameter: no division per tile)
+  int st = 0, rs = 0;  // stage of tile kt, stage of the tile refilled at kt (kt - lag)
+  unsigned ph = 0;     // mbarrier phase parity of tile kt
 
   const bool scaled = SCALED && jb.scale_sel >= 0;
+  // with the TMA-stored copy a stage is refilled one tile later (lag 2): the store of the tile just
+  // finished may still be reading its stage, the one before it must have finished (wait_group.read 1)
+  const bool cbulk = SCALED && jb.cbulk;
+  const int lag = cbulk ? 2 : 1;
   double acc = (OP != LN_ABS && jb.init && l0 + lane < jb.nlines) ? jb.init[l0 + lane] : 0.0;
 #pragma unroll 1
-  for (int64_t kt = 0; kt < KT; ++kt) {
-    if (kt >= 1) {
-      // refill tile kt-1's stage with tile kt-1+STAGES here, after the loop back edge: every op
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt >= lag) {
+      // refill tile kt-lag's stage with tile kt-lag+STAGES here, after the loop back edge: every op
       // consuming its shared-memory loads has issued, so those loads have completed (refilling
       // at the end of iteration kt-1 would let ptxas hoist the copy above in-flight loads)
-      const int64_t nk = kt - 1 + S;
+      const int nk = kt - lag + S;
       if (jb.bulk) fence_proxy_async_smem();
       __syncwarp();
       if (nk < KT) {
-        const int sp = int((kt - 1) % S);
-        ln_issue(L, ji, ln_smem + sp * LN_TILE, bars + sp, l0, nk, lane);
+        if (cbulk && lane == 0) bulk_wait_read<1>();
+        ln_issue(L, ji, ln_smem + rs * LN_TILE, bars + rs, l0, nk, lane);
       }
+      rs = rs + 1 == S ? 0 : rs + 1;
       __syncwarp();
     }
-    const int st = int(kt % S);
-    mbar_wait(bars + st, unsigned((kt / S) & 1));
+    mbar_wait(bars + st, ph);
     const double* t = ln_smem + st * LN_TILE;
-    const int64_t k0 = kt * LN_TK;
+    const int64_t k0 = int64_t(kt) * LN_TK;
     const int kv = int(jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK);
     if (jb.by_rows) {
       // lane = row l0 + lane; its 16-byte chunk q (columns 2q, 2q+1) sits in box q/8 at chunk (q%8)^(lane%8)
@@ -227,7 +238,19 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         // pairs (2q, 2q+1) of this tile that lie below pair_end
         const int64_t pe = jb.pair_end - k0;
         const int np = int((pe < kv ? pe : kv) / 2);
-        if (np == LN_TK / 2) {
+        if (cbulk) {
+          // scale the lane's row of the tile in place (the copy leaves from here by TMA store),
+          // then the pairs below pair_end on the scaled values: the same dmul(s, x) roundings
+          double* rw = ln_smem + st * LN_TILE + lane * 16;
+#pragma unroll
+          for (int q = 0; q < LN_TK / 2; ++q) {
+            double2* p2 = reinterpret_cast<double2*>(rw + (q >> 3) * (LN_LINES * 16) + (((q & 7) ^ (lane & 7)) << 1));
+            double2 v = *p2;
+            v = make_double2(dmul(s, v.x), dmul(s, v.y));
+            *p2 = v;
+            if (q < np) acc = ln_pair<OP>(acc, v.x, v.y);
+          }
+        } else if (np == LN_TK / 2) {
 #pragma unroll
           for (int q = 0; q < LN_TK / 2; ++q) {
             double2 v = chunk(q);
@@ -242,7 +265,15 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
           }
         }
       }
-      if (jb.copy) {  // coalesced write of the scaled tile: lane = column
+      if (cbulk) {  // the scaled tile leaves by TMA store (two 16-column boxes; the map clips edges)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&L.cmap[ji], int(k0), int(l0), t);
+          tma_store_2d(&L.cmap[ji], int(k0 + 16), int(l0), t + LN_LINES * 16);
+          bulk_commit();
+        }
+      } else if (jb.copy) {  // coalesced write of the scaled tile: lane = column
         const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
         if (lane < kv)
           for (int r = 0; r < lv; ++r) jb.copy[(l0 + r) * jb.ld + k0 + lane] = dmul(s, t[ln_rowoff(r, lane)]);
@@ -254,7 +285,16 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
       } else {
         const int64_t pe = jb.pair_end - k0;
         const int np = int((pe < kv ? pe : kv) / 2);
-        if (np == LN_TK / 2) {
+        if (cbulk) {  // scale the lane's column of the tile in place, pairs on the scaled values
+          double* cw = ln_smem + st * LN_TILE + lane;
+#pragma unroll
+          for (int j = 0; j < LN_TK / 2; ++j) {
+            const double x0 = dmul(s, cw[(2 * j) * LN_LINES]), x1 = dmul(s, cw[(2 * j + 1) * LN_LINES]);
+            cw[(2 * j) * LN_LINES] = x0;
+            cw[(2 * j + 1) * LN_LINES] = x1;
+            if (j < np) acc = ln_pair<OP>(acc, x0, x1);
+          }
+        } else if (np == LN_TK / 2) {
 #pragma unroll
           for (int j = 0; j < LN_TK / 2; ++j) {
             double x0 = t[(2 * j) * LN_LINES + lane], x1 = t[(2 * j + 1) * LN_LINES + lane];
@@ -275,14 +315,27 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
           }
         }
       }
-      if (jb.copy) {  // lane = column; rows of the panel are 256-byte coalesced stores
+      if (cbulk) {  // the scaled tile leaves by TMA store (the map clips the edges)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&L.cmap[ji], int(l0), int(k0), t);
+          bulk_commit();
+        }
+      } else if (jb.copy) {  // lane = column; rows of the panel are 256-byte coalesced stores
         const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
         if (lane < lv)
           for (int k = 0; k < kv; ++k) jb.copy[(k0 + k) * jb.ld + l0 + lane] = dmul(s, t[k * LN_LINES + lane]);
       }
     }
+    if (++st == S) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
 
+  if (cbulk && lane == 0) bulk_wait_all();  // the stores have left shared memory (and landed)
+  __syncwarp();
   const bool valid = l0 + lane < jb.nlines;
   if (OP == LN_ABS) {
     double m = valid ? acc : 0.0;  // max is order-free
@@ -298,15 +351,20 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
 }
 
 // fill the derived fields of a job (blocks; TMA map when the operand allows one)
-inline void ln_finish_job(LineJob& j, CUtensorMap* map) {
+inline void ln_finish_job(LineJob& j, CUtensorMap* map, CUtensorMap* cmap) {
   j.blocks = int(cdiv(j.nlines, LN_LINES));
   j.bulk = 0;
+  j.cbulk = 0;
   if (tma_ok(j.X, j.ld)) {
     const int64_t rows = j.by_rows ? j.nlines : j.len, cols = j.by_rows ? j.len : j.nlines;
     if (j.by_rows)
       j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_LINES, 16, true);
     else
       j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_TK, LN_LINES, false);
+    // the copy has X's shape and pitch: the same box geometry stores the (in place scaled) tile
+    if (j.bulk && j.copy && j.scale_sel >= 0 && tma_ok(j.copy, j.ld))
+      j.cbulk = j.by_rows ? tma_encode_2d(cmap, j.copy, rows, cols, j.ld, LN_LINES, 16, true)
+                          : tma_encode_2d(cmap, j.copy, rows, cols, j.ld, LN_TK, LN_LINES, false);
   }
 }
 
@@ -316,7 +374,7 @@ inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   int blocks = 0;
   for (int i = 0; i < L.njobs; ++i) {
-    ln_finish_job(L.job[i], &L.map[i]);
+    ln_finish_job(L.job[i], &L.map[i], &L.cmap[i]);
     blocks += L.job[i].blocks;
   }
   // ring depth: the shared memory of an SM (~220 KB usable) shared by the blocks it will hold

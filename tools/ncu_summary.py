@@ -23,7 +23,7 @@ def family(name: str) -> str:
         return "line_kernel<0> (norm_inf)"
     if "line_kernel<1" in name or "line_kernel<2" in name:
         return "line_kernel<1> (winograd y/z)"
-    for k in ("dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_tma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
+    for k in ("dgemm_tma_comb_kernel", "dgemm_tma_kernel", "dgemm_dmma_kernel", "kahan_tma_kernel", "kahan_gemm_kernel", "winograd_yz_kernel", "winograd_tma_kernel",
               "winograd_kernel",
               "strassen_form3_kernel", "strassen_form2_kernel", "strassen_combine2_kernel",
               "strassen_form_kernel", "strassen_combine_kernel", "norm_inf_kernel", "scale_copy_kernel",
@@ -74,7 +74,7 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12
 
 def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "profiles", "r01")):
     os.makedirs(dst, exist_ok=True)
-    md = ["# ncu summary (round 1)", ""]
+    md = [f"# ncu summary ({os.path.basename(os.path.normpath(dst))})", ""]
     L = launches(os.path.join(src, "launches.csv"))
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d in L:
@@ -129,7 +129,7 @@ def main(src=os.path.join(ROOT, "gpurun_out", "ncu"), dst=os.path.join(ROOT, "pr
             key = (d["ID"], short(d["Kernel Name"]), d["Grid Size"])
             v = float(d["Metric Value"].replace(",", "")) * UNIT_SCALE.get(d["Metric Unit"], 1)
             per[key][d["Metric Name"]] = v
-        md += ["", "## HBM-bound kernels (winograd_scaled + strassen_winograd d=2 at c4)", "",
+        md += ["", "## HBM-bound kernels (winograd_scaled + strassen_winograd at c4)", "",
                "| id | kernel | grid | time ms | DRAM read GB | DRAM write GB | achieved GB/s | dram % |", "|---|---|---|---|---|---|---|---|"]
         for (i, k, grid), m in sorted(per.items(), key=lambda x: int(x[0][0])):
             t = m.get("gpu__time_duration.sum", 0)
