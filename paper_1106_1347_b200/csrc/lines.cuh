@@ -13,7 +13,7 @@
 //   * one warp = 32 lines, one warp per CTA, a shared-memory ring of LN_STAGES (6) to
 //     LN_MAX_STAGES (24) stages -- deeper when the grid leaves SMs to spare (a 1024-row shard of
 //     A is only 32 warps: each then keeps 24 x 8 KB in flight instead of 6 x 8 KB) -- of
-//     32 x LN_TK tiles;
+//     32 x LN_TK (32, or LN_TK_LONG = 128 when the launch has few lines) tiles;
 //   * operands with a 16-byte aligned base and even pitch arrive by TMA (2-D tensor maps,
 //     one elected lane issues the tile's box copies, completion counted in bytes on an
 //     mbarrier); 8-byte aligned operands (odd pitch, e.g. P = 1001) fall back to 8-byte
@@ -42,9 +42,13 @@ namespace mmk {
 constexpr int LN_LINES = 32, LN_TK = 32, LN_STAGES = 6, LN_MAX_STAGES = 24;
 constexpr int LN_TILE = LN_LINES * LN_TK;  // 8 KB per stage
 constexpr unsigned LN_TILE_BYTES = LN_TILE * sizeof(double);
-inline constexpr size_t ln_smem(int stages) {
-  return 1024 + size_t(stages) * LN_TILE * sizeof(double) + stages * sizeof(uint64_t);
+inline constexpr size_t ln_smem(int stages, int tk = LN_TK) {
+  return 1024 + size_t(stages) * LN_LINES * tk * sizeof(double) + stages * sizeof(uint64_t);
 }
+// Long tiles (TK = 128) for launches with few lines: a line's chain costs 8 cycles per element
+// (FP64 latency, tools/probes/lat_probe.cu) plus a fixed cost per tile (barrier wait, refill,
+// fences) that a warp alone on its SM cannot hide; 4x longer tiles amortise it 4x.
+constexpr int LN_TK_LONG = 128, LN_TK_MID = 64;
 static_assert(LN_TK == 32 && LN_LINES == 32, "one lane per tile column / line");
 
 // LN_PAIRS_FMA: the NEXT-3 fused variant (reading R22), y = fma(x0, x1, y)
@@ -109,32 +113,37 @@ __device__ __forceinline__ int ln_rowoff(int r, int c) {
 }
 
 // issue the copies of tile kt of block-lines [l0, l0+32) into stage buffer t (barrier bar)
+template <int TK>
 __device__ __forceinline__ void ln_issue(const LineLaunch& L, int ji, double* t, uint64_t* bar, int64_t l0,
                                          int64_t kt, int lane) {
   const LineJob& jb = L.job[ji];
-  const int64_t k0 = kt * LN_TK;
+  const int64_t k0 = kt * TK;
   if (jb.bulk) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(bar, LN_TILE_BYTES);
+      mbar_arrive_expect_tx(bar, unsigned(LN_LINES * TK * sizeof(double)));
       if (jb.by_rows) {
-        tma_load_2d(t, &L.map[ji], int(k0), int(l0), bar);
-        tma_load_2d(t + LN_LINES * 16, &L.map[ji], int(k0 + 16), int(l0), bar);
+#pragma unroll
+        for (int bx = 0; bx < TK / 16; ++bx)  // [32 rows][16 columns] boxes
+          tma_load_2d(t + bx * (LN_LINES * 16), &L.map[ji], int(k0 + 16 * bx), int(l0), bar);
       } else {
         tma_load_2d(t, &L.map[ji], int(l0), int(k0), bar);
       }
     }
   } else {
-    const int64_t kv = jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK;              // valid elements along the line
+    const int64_t kv = jb.len - k0 < TK ? jb.len - k0 : TK;              // valid elements along the line
     const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;  // valid lines
     if (jb.by_rows) {
 #pragma unroll 8
       for (int r = 0; r < LN_LINES; ++r) {
-        const bool v = r < lv && lane < kv;
-        cp_async8(t + ln_rowoff(r, lane), v ? jb.X + (l0 + r) * jb.ld + k0 + lane : jb.X, v);
+#pragma unroll
+        for (int c = lane; c < TK; c += 32) {
+          const bool v = r < lv && c < kv;
+          cp_async8(t + ln_rowoff(r, c), v ? jb.X + (l0 + r) * jb.ld + k0 + c : jb.X, v);
+        }
       }
     } else {
 #pragma unroll 8
-      for (int k = 0; k < LN_TK; ++k) {
+      for (int k = 0; k < TK; ++k) {
         const bool v = k < kv && lane < lv;
         cp_async8(t + k * LN_LINES + lane, v ? jb.X + (k0 + k) * jb.ld + l0 + lane : jb.X, v);
       }
@@ -145,13 +154,13 @@ __device__ __forceinline__ void ln_issue(const LineLaunch& L, int ji, double* t,
 
 // SCALED: the jobs carry scale_sel >= 0 (WinogradScaled's copies); a compile-time flag so the
 // unscaled y/z pass executes exactly the method's DMUL/DADD (SASS fingerprint, tools/fingerprint.py)
-template <int OP, bool SCALED>
+template <int OP, bool SCALED, int TK>
 __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ LineLaunch L) {
   extern __shared__ __align__(1024) unsigned char ln_raw[];
   // 1024-byte aligned stage buffers (the 128-byte swizzle pattern repeats every 1024 bytes)
   double* ln_smem = reinterpret_cast<double*>(ln_raw + ((1024 - (smem_u32(ln_raw) & 1023)) & 1023));
   const int S = L.stages;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ln_smem + S * LN_TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ln_smem + S * (LN_LINES * TK));
   const int lane = threadIdx.x;
   int b = blockIdx.x, ji = 0;
   if (L.njobs > 1 && b >= L.job[0].blocks) {
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   }
   const LineJob& jb = L.job[ji];
   const int64_t l0 = int64_t(b) * LN_LINES;
-  const int KT = int(cdiv(jb.len, LN_TK));
+  const int KT = int(cdiv(jb.len, TK));
 
   double s = 1.0;
   if (SCALED && jb.scale_sel >= 0) {
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
   __syncwarp();
 #pragma unroll 1
   for (int st = 0; st < S; ++st)
-    if (st < KT) ln_issue(L, ji, ln_smem + st * LN_TILE, bars + st, l0, st, lane);
+    if (st < KT) ln_issue<TK>(L, ji, ln_smem + st * (LN_LINES * TK), bars + st, l0, st, lane);
   // ring positions kept incrementally (S is a launch parameter: no division per tile)
   int st = 0, rs = 0;  // stage of tile kt, stage of the tile refilled at kt (kt - lag)
   unsigned ph = 0;     // mbarrier phase parity of tile kt
@@ -208,15 +217,15 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
       __syncwarp();
       if (nk < KT) {
         if (cbulk && lane == 0) bulk_wait_read<1>();
-        ln_issue(L, ji, ln_smem + rs * LN_TILE, bars + rs, l0, nk, lane);
+        ln_issue<TK>(L, ji, ln_smem + rs * (LN_LINES * TK), bars + rs, l0, nk, lane);
       }
       rs = rs + 1 == S ? 0 : rs + 1;
       __syncwarp();
     }
     mbar_wait(bars + st, ph);
-    const double* t = ln_smem + st * LN_TILE;
-    const int64_t k0 = int64_t(kt) * LN_TK;
-    const int kv = int(jb.len - k0 < LN_TK ? jb.len - k0 : LN_TK);
+    const double* t = ln_smem + st * (LN_LINES * TK);
+    const int64_t k0 = int64_t(kt) * TK;
+    const int kv = int(jb.len - k0 < TK ? jb.len - k0 : TK);
     if (jb.by_rows) {
       // lane = row l0 + lane; its 16-byte chunk q (columns 2q, 2q+1) sits in box q/8 at chunk (q%8)^(lane%8)
       const double* row = t + lane * 16;
@@ -224,9 +233,9 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         return *reinterpret_cast<const double2*>(row + (q >> 3) * (LN_LINES * 16) + (((q & 7) ^ (lane & 7)) << 1));
       };
       if (OP == LN_ABS) {
-        if (kv == LN_TK) {
+        if (kv == TK) {
 #pragma unroll
-          for (int q = 0; q < LN_TK / 2; ++q) {
+          for (int q = 0; q < TK / 2; ++q) {
             const double2 v = chunk(q);
             acc = dadd(acc, fabs(v.x));  // row sum, left to right
             acc = dadd(acc, fabs(v.y));
@@ -241,18 +250,18 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         if (cbulk) {
           // scale the lane's row of the tile in place (the copy leaves from here by TMA store),
           // then the pairs below pair_end on the scaled values: the same dmul(s, x) roundings
-          double* rw = ln_smem + st * LN_TILE + lane * 16;
+          double* rw = ln_smem + st * (LN_LINES * TK) + lane * 16;
 #pragma unroll
-          for (int q = 0; q < LN_TK / 2; ++q) {
+          for (int q = 0; q < TK / 2; ++q) {
             double2* p2 = reinterpret_cast<double2*>(rw + (q >> 3) * (LN_LINES * 16) + (((q & 7) ^ (lane & 7)) << 1));
             double2 v = *p2;
             v = make_double2(dmul(s, v.x), dmul(s, v.y));
             *p2 = v;
             if (q < np) acc = ln_pair<OP>(acc, v.x, v.y);
           }
-        } else if (np == LN_TK / 2) {
+        } else if (np == TK / 2) {
 #pragma unroll
-          for (int q = 0; q < LN_TK / 2; ++q) {
+          for (int q = 0; q < TK / 2; ++q) {
             double2 v = chunk(q);
             if (scaled) v = make_double2(dmul(s, v.x), dmul(s, v.y));
             acc = ln_pair<OP>(acc, v.x, v.y);  // y_i += A[i][2j] A[i][2j+1]
@@ -269,8 +278,9 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&L.cmap[ji], int(k0), int(l0), t);
-          tma_store_2d(&L.cmap[ji], int(k0 + 16), int(l0), t + LN_LINES * 16);
+#pragma unroll
+          for (int bx = 0; bx < TK / 16; ++bx)
+            tma_store_2d(&L.cmap[ji], int(k0 + 16 * bx), int(l0), t + bx * (LN_LINES * 16));
           bulk_commit();
         }
       } else if (jb.copy) {  // coalesced write of the scaled tile: lane = column
@@ -286,17 +296,17 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
         const int64_t pe = jb.pair_end - k0;
         const int np = int((pe < kv ? pe : kv) / 2);
         if (cbulk) {  // scale the lane's column of the tile in place, pairs on the scaled values
-          double* cw = ln_smem + st * LN_TILE + lane;
+          double* cw = ln_smem + st * (LN_LINES * TK) + lane;
 #pragma unroll
-          for (int j = 0; j < LN_TK / 2; ++j) {
+          for (int j = 0; j < TK / 2; ++j) {
             const double x0 = dmul(s, cw[(2 * j) * LN_LINES]), x1 = dmul(s, cw[(2 * j + 1) * LN_LINES]);
             cw[(2 * j) * LN_LINES] = x0;
             cw[(2 * j + 1) * LN_LINES] = x1;
             if (j < np) acc = ln_pair<OP>(acc, x0, x1);
           }
-        } else if (np == LN_TK / 2) {
+        } else if (np == TK / 2) {
 #pragma unroll
-          for (int j = 0; j < LN_TK / 2; ++j) {
+          for (int j = 0; j < TK / 2; ++j) {
             double x0 = t[(2 * j) * LN_LINES + lane], x1 = t[(2 * j + 1) * LN_LINES + lane];
             if (scaled) {
               x0 = dmul(s, x0);
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
 }
 
 // fill the derived fields of a job (blocks; TMA map when the operand allows one)
-inline void ln_finish_job(LineJob& j, CUtensorMap* map, CUtensorMap* cmap) {
+inline void ln_finish_job(LineJob& j, CUtensorMap* map, CUtensorMap* cmap, int tk) {
   j.blocks = int(cdiv(j.nlines, LN_LINES));
   j.bulk = 0;
   j.cbulk = 0;
@@ -360,24 +370,39 @@ inline void ln_finish_job(LineJob& j, CUtensorMap* map, CUtensorMap* cmap) {
     if (j.by_rows)
       j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_LINES, 16, true);
     else
-      j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_TK, LN_LINES, false);
+      j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, tk, LN_LINES, false);
     // the copy has X's shape and pitch: the same box geometry stores the (in place scaled) tile
     if (j.bulk && j.copy && j.scale_sel >= 0 && tma_ok(j.copy, j.ld))
       j.cbulk = j.by_rows ? tma_encode_2d(cmap, j.copy, rows, cols, j.ld, LN_LINES, 16, true)
-                          : tma_encode_2d(cmap, j.copy, rows, cols, j.ld, LN_TK, LN_LINES, false);
+                          : tma_encode_2d(cmap, j.copy, rows, cols, j.ld, tk, LN_LINES, false);
   }
+}
+
+template <int OP, bool SCALED, int TK>
+inline cudaError_t launch_lines_tk(LineLaunch& L, int blocks, int sms, cudaStream_t st) {
+  constexpr auto k = line_kernel<OP, SCALED, TK>;
+  constexpr int tile = LN_LINES * TK * int(sizeof(double)) + 8;
+  constexpr int smax = (220 * 1024 - 1024) / tile < LN_MAX_STAGES ? (220 * 1024 - 1024) / tile : LN_MAX_STAGES;
+  cudaError_t e = smem_attr_once<k>(ln_smem(smax, TK));
+  if (e != cudaSuccess) return e;
+  // ring depth: the shared memory of an SM (~220 KB usable) shared by the blocks it will hold
+  const int per_sm = int((blocks + sms - 1) / sms);
+  int stages = int((220 * 1024 / (per_sm > 0 ? per_sm : 1) - 1024) / tile);
+  if (stages > smax) stages = smax;
+  static const int cap = [] {  // MM_LN_MAX_STAGES: tuning override of the depth cap
+    const char* v = std::getenv("MM_LN_MAX_STAGES");
+    const int c = v ? std::atoi(v) : LN_MAX_STAGES;
+    return c < 2 ? 2 : (c > LN_MAX_STAGES ? LN_MAX_STAGES : c);
+  }();
+  const int lo = TK == LN_TK ? LN_STAGES : 3;
+  L.stages = stages < lo ? lo : (stages > cap ? cap : stages);
+  k<<<unsigned(blocks), LN_LINES, ln_smem(L.stages, TK), st>>>(L);
+  note_launch();
+  return cudaGetLastError();
 }
 
 template <int OP, bool SCALED = false>
 inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
-  cudaError_t e = smem_attr_once<line_kernel<OP, SCALED>>(ln_smem(LN_MAX_STAGES));
-  if (e != cudaSuccess) return e;
-  int blocks = 0;
-  for (int i = 0; i < L.njobs; ++i) {
-    ln_finish_job(L.job[i], &L.map[i], &L.cmap[i]);
-    blocks += L.job[i].blocks;
-  }
-  // ring depth: the shared memory of an SM (~220 KB usable) shared by the blocks it will hold
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -387,17 +412,19 @@ inline cudaError_t launch_lines(LineLaunch& L, cudaStream_t st) {
       sms = 148;
     }
   }
-  const int per_sm = int((blocks + sms - 1) / sms);
-  int stages = int((220 * 1024 / (per_sm > 0 ? per_sm : 1) - 1024) / (LN_TILE * sizeof(double) + 8));
-  static const int cap = [] {  // MM_LN_MAX_STAGES: tuning override of the depth cap (6 .. 24)
-    const char* e = std::getenv("MM_LN_MAX_STAGES");
-    const int v = e ? std::atoi(e) : LN_MAX_STAGES;
-    return v < LN_STAGES ? LN_STAGES : (v > LN_MAX_STAGES ? LN_MAX_STAGES : v);
-  }();
-  L.stages = stages < LN_STAGES ? LN_STAGES : (stages > cap ? cap : stages);
-  line_kernel<OP, SCALED><<<unsigned(blocks), LN_LINES, ln_smem(L.stages), st>>>(L);
-  note_launch();
-  return cudaGetLastError();
+  // longer tiles the fewer blocks an SM holds, when every operand streams by TMA: 128-element
+  // tiles up to two blocks per SM (3-6 stages of 32 KB), 64-element tiles up to four (3 of 16 KB)
+  int blocks = 0;
+  bool all_tma = true;
+  for (int i = 0; i < L.njobs; ++i) {
+    blocks += int(cdiv(L.job[i].nlines, LN_LINES));
+    all_tma = all_tma && tma_ok(L.job[i].X, L.job[i].ld);
+  }
+  const int tk = !all_tma ? LN_TK : blocks <= 2 * sms ? LN_TK_LONG : blocks <= 4 * sms ? LN_TK_MID : LN_TK;
+  for (int i = 0; i < L.njobs; ++i) ln_finish_job(L.job[i], &L.map[i], &L.cmap[i], tk);
+  if (tk == LN_TK_LONG) return launch_lines_tk<OP, SCALED, LN_TK_LONG>(L, blocks, sms, st);
+  if (tk == LN_TK_MID) return launch_lines_tk<OP, SCALED, LN_TK_MID>(L, blocks, sms, st);
+  return launch_lines_tk<OP, SCALED, LN_TK>(L, blocks, sms, st);
 }
 
 inline LineJob ln_job(const double* X, int64_t ld, int64_t nlines, int64_t len, bool by_rows, int op) {
