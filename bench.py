@@ -530,8 +530,9 @@ def run_e2e(args, methods, A_h, B_h, dev, world, rank, n_loc, P, M, native=None)
     d2h = len(methods) * 8 * n_loc * M
     return {"value": round(flop / (ms / 1e3) / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": steps,
-            "path": "paper_1106_1347_b200.matmul_methods on pinned host tensors (per step: H2D A, B once, in k-panels "
-                    "that NaivStandard consumes as they land; every method's C D2H, overlapped with the next method)"
+            "path": "C ABI mm_methods_host (via paper_1106_1347_b200.matmul_methods) on pinned host buffers: per step "
+                    "H2D of A and B once, in k-panels that NaivStandard consumes as they land; every method's C D2H, "
+                    "overlapped with the next method"
             if world == 1 else "dist_gemm: per step H2D of each rank's A rows (+ B on the root) once, every method's "
                                "C rows D2H"}
 

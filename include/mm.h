@@ -180,6 +180,29 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
             int32_t levels, void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream);
 
 /*
+ * mm_methods_host -- the paper's test program from HOST memory: C_host[i] = A B by
+ * methods[i], i < n, all on the same operands.  A_host (N x P), B_host (P x M) and every C_host[i]
+ * (N x M) are HOST pointers, row-major float64 (page-locked memory lets the copies overlap the
+ * kernels; pageable memory works but the copies then serialise).  A and B are copied to the device
+ * once; the methods run in turn on `stream`; each product is copied back on a library-owned copy
+ * stream while the next method computes.  A first NaivStandard multiplies k-panels of A and B as
+ * they land (mm_naive_ex accumulation, bitwise the one-shot product); a first row-local method
+ * (NaivKahan, WinogradOriginal and their fused variants) starts on each of `row_blocks` row blocks
+ * of A as it lands; a last row-local method returns its product by row blocks of halving height.
+ * Every C_host[i] equals the device entry point's result bit for bit.  levels: for the Strassen
+ * methods (as mm_strassen).  dev_ws: DEVICE workspace of at least
+ * mm_methods_host_workspace_size(methods, n, N, P, M, levels) bytes (device copies of A and B, two
+ * product buffers, the largest method workspace).  SYNCHRONOUS: returns once every product has
+ * landed in host memory.  The library keeps two copy streams per device for these calls.
+ * Errors as mm_gemm; MM_ERR_ARG for a NULL C_host[i] or an unknown method id.
+ */
+size_t mm_methods_host_workspace_size(const int* methods, int32_t n, int64_t N, int64_t P, int64_t M,
+                                      int32_t levels);
+int mm_methods_host(const int* methods, int32_t n, const double* A_host, const double* B_host, double* const* C_host,
+                    int64_t N, int64_t P, int64_t M, int32_t levels, int32_t row_blocks, void* dev_ws, size_t ws_bytes,
+                    void* stream);
+
+/*
  * norm_inf -- ||X||_inf = max_i sum_j |X_ij| of a dense row-major rows x cols
  * device matrix; each row sum is accumulated left to right (as the oracle does), the max
  * is order-free.  out_device: DEVICE pointer to one double, overwritten.

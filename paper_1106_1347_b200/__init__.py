@@ -45,7 +45,7 @@ EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winogra
            "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
            "mm_winograd_scaled_fused", "mm_naive_ex", "mm_dist_get_unique_id", "mm_dist_init",
            "mm_dist_workspace_size", "mm_dist_gemm", "mm_dist_finalize", "mm_kahan_ex", "mm_winograd_ex",
-           "mm_winograd_yz", "mm_dist_schedule", "mm_dist_step")
+           "mm_winograd_yz", "mm_dist_schedule", "mm_dist_step", "mm_methods_host", "mm_methods_host_workspace_size")
 MM_EX_ACCUMULATE, MM_EX_KEEP_STATE, MM_EX_FUSED = 1, 2, 4
 
 
@@ -80,6 +80,9 @@ def lib() -> ctypes.CDLL:
         L.mm_dist_workspace_size.restype = sz
         L.mm_dist_gemm.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64, i32, i32, i32, vp, sz, vp]
         L.mm_dist_schedule.argtypes = [ctypes.c_int, i64, i64, i32, i32, vp, i32]
+        L.mm_methods_host_workspace_size.argtypes = [vp, i32, i64, i64, i64, i32]
+        L.mm_methods_host_workspace_size.restype = sz
+        L.mm_methods_host.argtypes = [vp, i32, dp, dp, vp, i64, i64, i64, i32, i32, vp, sz, vp]
         L.mm_dist_step.argtypes = [ctypes.c_int, vp, dp, dp, dp, i64, i64, i64, i32, i32, vp, sz, vp]
         for n in ("mm_winograd", "mm_winograd_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
@@ -379,220 +382,68 @@ _FUNCS = {
 # methods whose entries depend only on (row of A, column of B): a row block of C is computed
 # bit-identically from the matching row block of A, so host copies can be pipelined by rows
 _ROW_LOCAL = ("naive", "kahan", "winograd", "kahan_fused", "winograd_fused")
-_STREAMS = {}
-
-
-def _aux_streams(dev):
-    key = dev.index
-    if key not in _STREAMS:
-        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _STREAMS[key]
-
-
 def matmul(A: torch.Tensor, B: torch.Tensor, method: str = "naive", *, levels: int = 2, device=None,
            stream=None, out: Optional[torch.Tensor] = None, row_blocks: int = 4) -> torch.Tensor:
-    """The user-level call.  Device tensors run in place on their device; host tensors are
-    copied to `device` (default cuda:current), multiplied there and the product is copied back
-    into `out` (or a new host tensor) -- the end-to-end path bench.py's `e2e` times.
-
-    For the row-local methods (NaivStandard, NaivKahan, WinogradOriginal) with pinned host
-    tensors, A and C move in `row_blocks` row blocks on two copy streams so the host<->device
-    transfers overlap the kernels; each block's entries are computed by the same kernel
-    arithmetic, so the result is bitwise the one-shot product."""
+    """The user-level call.  Device tensors run in place on their device; host tensors go through
+    the C ABI's host-buffer entry point (mm_methods_host with one method): copied to `device`
+    (default cuda:current), multiplied, the product copied back into `out` (or a new host tensor),
+    with A's row blocks / k-panels pipelined against the kernels for page-locked tensors.  Bitwise
+    the device call's result."""
     f = _FUNCS[method]
     kw = {"levels": levels} if method in ("strassen", "strassen_winograd") else {}
     if A.is_cuda and B.is_cuda:
         return f(A, B, out=out, stream=stream, **kw)
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    N, M = A.shape[0], B.shape[1]
     if out is None:
-        out = torch.empty((N, M), dtype=torch.float64, pin_memory=A.is_pinned())
-    pipelined = (method in _ROW_LOCAL and row_blocks > 1 and N >= 2 * row_blocks and A.is_pinned()
-                 and out.is_pinned())
-    if not pipelined:
-        with torch.cuda.stream(s):
-            dA = A.to(dev, non_blocking=True)
-            dB = B.to(dev, non_blocking=True)
-            dC = f(dA, dB, stream=s, **kw)
-            out.copy_(dC, non_blocking=True)
-        s.synchronize()
-        return out
-    s_in, s_out = _aux_streams(dev)
-    s_in.wait_stream(s)
-    bounds = [(N * b) // row_blocks for b in range(row_blocks + 1)]
-    with torch.cuda.stream(s_in):
-        dB = B.to(dev, non_blocking=True)
-        dA = torch.empty(A.shape, dtype=torch.float64, device=dev)
-    dC = torch.empty((N, M), dtype=torch.float64, device=dev)
-    for b in range(row_blocks):
-        lo, hi = bounds[b], bounds[b + 1]
-        with torch.cuda.stream(s_in):
-            dA[lo:hi].copy_(A[lo:hi], non_blocking=True)
-        s.wait_stream(s_in)
-        f(dA[lo:hi], dB, out=dC[lo:hi], stream=s)
-        s_out.wait_stream(s)
-        with torch.cuda.stream(s_out):
-            out[lo:hi].copy_(dC[lo:hi], non_blocking=True)
-    for t in (dA, dB, dC):
-        t.record_stream(s_in)
-        t.record_stream(s)
-        t.record_stream(s_out)
-    s_out.synchronize()
-    s.synchronize()
+        out = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, pin_memory=A.is_pinned())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            matmul_methods(A.contiguous(), B.contiguous(), [method], levels=levels, device=dev, outs={method: out},
+                           row_blocks=row_blocks)
+    else:
+        matmul_methods(A.contiguous(), B.contiguous(), [method], levels=levels, device=dev, outs={method: out},
+                       row_blocks=row_blocks)
     return out
-
-
-def _h2d_2d(dA: torch.Tensor, hA: torch.Tensor, k0: int, k1: int, stream) -> None:
-    """dA[:, k0:k1] <- hA[:, k0:k1] (pinned host, row-major) as ONE strided 2-D copy on `stream`
-    (cudaMemcpy2DAsync through the CUDA runtime bindings; torch would gather a strided pinned
-    source through a pageable temporary, which is synchronous)."""
-    from cuda.bindings import runtime as rt
-
-    pitch = hA.stride(0) * 8
-    err, = rt.cudaMemcpy2DAsync(dA.data_ptr() + k0 * 8, dA.stride(0) * 8, hA.data_ptr() + k0 * 8, pitch,
-                                (k1 - k0) * 8, hA.shape[0], rt.cudaMemcpyKind.cudaMemcpyHostToDevice,
-                                stream.cuda_stream)
-    if err != rt.cudaError_t.cudaSuccess:
-        raise MMError(f"cudaMemcpy2DAsync failed: {err}")
-
-
-def _growing_panels(P: int, n: int, ratio: float = 1.4):
-    """n consecutive k-panels of P with even boundaries whose widths grow by `ratio`: the first
-    panel's host->device copy is all the product waits for, and each later copy (A's columns and
-    B's rows, ~2.6 us per k at c4 over PCIe) hides under the previous panel's DMMA work (~3.7 us
-    per k), which grows ~1.4x faster than the copy."""
-    n = max(1, min(n, P // 2 if P >= 2 else 1))
-    w = [ratio ** i for i in range(n)]
-    tot = sum(w)
-    cuts, acc = [], 0.0
-    for x in w[:-1]:
-        acc += x
-        c = 2 * int(round(P * acc / tot / 2))
-        if (not cuts or c > cuts[-1]) and 0 < c < P:
-            cuts.append(c)
-    b = [0] + cuts + [P]
-    return list(zip(b[:-1], b[1:]))
-
-
-def _shrinking_rows(N: int, n: int, quantum: int = 64, min_rows: int = 1024):
-    """At most n row blocks of N halving in size (multiples of `quantum` rows, the SIMT kernels'
-    tile height; none below `min_rows`, which still fills the GPU): the device->host copy of every
-    block but the last hides under the next block's kernel, and the last block -- the only copy
-    left after the final kernel -- is small.  min_rows = 1024: blocks of a few waves lose more to
-    their partial last wave than the smaller final copy saves (profiles/r01/e2e_schedule.jsonl)."""
-    if n <= 1 or N < 2 * min_rows:
-        return [(0, N)]
-    sizes, rest = [], N
-    for _ in range(n - 1):
-        sz = max(quantum, (rest // 2) // quantum * quantum)
-        if rest - sz < min_rows:
-            break
-        sizes.append(sz)
-        rest -= sz
-    sizes.append(rest)
-    b = [0]
-    for sz in sizes:
-        b.append(b[-1] + sz)
-    return list(zip(b[:-1], b[1:]))
 
 
 def matmul_methods(A: torch.Tensor, B: torch.Tensor, methods, *, levels: int = 2, device=None,
                    outs: Optional[dict] = None, row_blocks: int = 4) -> dict:
     """The shape of the paper's test program: several methods applied to the
-    SAME host operands.  A and B (pinned host float64) are copied to the device once; every
-    method's product is copied back into outs[method] (pinned host, allocated if missing) on a
-    copy stream while the next method computes.  When the first method is NaivStandard, A and B
-    travel in k-panels of growing width (A's column panels as 2-D copies) and the product
-    accumulates panel by panel as they land (mm_naive_ex, reading R23: bitwise the one-shot
-    chain); when it is another row-local method its row blocks start as soon as their rows of A
-    have landed.  When the last method is row-local its result streams back by row blocks of
-    shrinking height.  Each product is bitwise the
-    one-shot device call's."""
+    SAME host operands, through the C ABI's host-buffer entry point ``mm_methods_host``: A and B
+    (host float64; page-locked for the copies to overlap) are copied to the device once, every
+    method's product comes back into outs[method] (page-locked host tensors, allocated if missing;
+    several methods may share one) while the next method computes.  A first NaivStandard
+    multiplies k-panels as they land, a first row-local method row blocks as they land, a last
+    row-local method returns by row blocks of halving height.  Each product is bitwise the device
+    call's.  Synchronous."""
     methods = list(methods)
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    s = torch.cuda.current_stream(dev)
-    s_in, s_out = _aux_streams(dev)
+    for X in (A, B):
+        if X.is_cuda or X.dtype != torch.float64 or X.dim() != 2 or not X.is_contiguous():
+            raise ValueError("A and B must be contiguous float64 host matrices")
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"inner dimensions differ: {tuple(A.shape)} x {tuple(B.shape)}")
     N, P = A.shape
     M = B.shape[1]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     outs = {} if outs is None else outs
     for m in methods:
         if m not in outs:
             outs[m] = torch.empty((N, M), dtype=torch.float64, pin_memory=True)
-    rb = max(1, min(row_blocks, N // 2)) if N >= 2 else 1
-    bounds = [(N * b) // rb for b in range(rb + 1)]
-    k_panels = None
-    if methods and methods[0] == "naive" and A.is_pinned() and B.is_pinned() and A.is_contiguous() and P >= 4:
-        k_panels = _growing_panels(P, row_blocks)
-    tail = _shrinking_rows(N, row_blocks)  # the last method's row blocks (see below)
-    s_in.wait_stream(s)
-    with torch.cuda.stream(s_in):
-        dA = torch.empty((N, P), dtype=torch.float64, device=dev)
-        dB = torch.empty((P, M), dtype=torch.float64, device=dev)
-        a_ready = []
-        if k_panels is not None:
-            for k0, k1 in k_panels:  # A[:, k0:k1] (strided) and B[k0:k1] (contiguous)
-                _h2d_2d(dA, A, k0, k1, s_in)
-                dB[k0:k1].copy_(B[k0:k1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(s_in)
-                a_ready.append(ev)
-        else:
-            dB.copy_(B, non_blocking=True)
-            for b in range(rb):
-                lo, hi = bounds[b], bounds[b + 1]
-                dA[lo:hi].copy_(A[lo:hi], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(s_in)
-                a_ready.append(ev)
-    bufs = [torch.empty((N, M), dtype=torch.float64, device=dev) for _ in range(min(2, len(methods)))]
-    buf_free = [None] * len(bufs)
-    for i, m in enumerate(methods):
-        f = _FUNCS[m]
-        kw = {"levels": levels} if m in ("strassen", "strassen_winograd") else {}
-        k = i % len(bufs)
-        if buf_free[k] is not None:
-            s.wait_event(buf_free[k])  # the D2H of the product that last used this buffer is done
-        buf = bufs[k]
-        row_local = m in _ROW_LOCAL and rb > 1
-        first, last = i == 0, i == len(methods) - 1
-        if first and k_panels is not None:  # NaivStandard accumulating k-panels as they land
-            for j, (k0, k1) in enumerate(k_panels):
-                s.wait_event(a_ready[j])
-                naive_panel(dA[:, k0:k1], dB[k0:k1], buf, accumulate=j > 0, stream=s)
-            s_out.wait_stream(s)
-            with torch.cuda.stream(s_out):
-                outs[m].copy_(buf, non_blocking=True)
-        elif row_local and first:  # its row blocks start as their rows of A land
-            for b in range(rb):
-                lo, hi = bounds[b], bounds[b + 1]
-                s.wait_event(a_ready[b] if k_panels is None else a_ready[-1])
-                f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
-                s_out.wait_stream(s)
-                with torch.cuda.stream(s_out):
-                    outs[m][lo:hi].copy_(buf[lo:hi], non_blocking=True)
-        elif row_local and last:  # shrinking row blocks: only the small last block's copy is exposed
-            s.wait_event(a_ready[-1])
-            for lo, hi in tail:
-                f(dA[lo:hi], dB, out=buf[lo:hi], stream=s, **kw)
-                s_out.wait_stream(s)
-                with torch.cuda.stream(s_out):
-                    outs[m][lo:hi].copy_(buf[lo:hi], non_blocking=True)
-        else:
-            s.wait_event(a_ready[-1])
-            f(dA, dB, out=buf, stream=s, **kw)
-            s_out.wait_stream(s)
-            with torch.cuda.stream(s_out):
-                outs[m].copy_(buf, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(s_out)
-        buf_free[k] = ev
-    for t in [dA, dB] + bufs:
-        t.record_stream(s_in)
-        t.record_stream(s)
-        t.record_stream(s_out)
-    s_out.synchronize()
-    s.synchronize()
+        o = outs[m]
+        if o.is_cuda or o.dtype != torch.float64 or tuple(o.shape) != (N, M) or not o.is_contiguous():
+            raise ValueError(f"outs[{m!r}] must be a contiguous float64 host tensor of shape {(N, M)}")
+    ids = (ctypes.c_int * len(methods))(*[METHODS[m] for m in methods])
+    L = lib()
+    nbytes = int(L.mm_methods_host_workspace_size(ids, len(methods), N, P, M, levels))
+    if nbytes == 0:
+        raise MMError("mm_methods_host_workspace_size: bad arguments")
+    s = torch.cuda.current_stream(dev)
+    ws_ptr, ws_len = _workspace(nbytes, dev, s)
+    cs = (ctypes.c_void_p * len(methods))(*[outs[m].data_ptr() for m in methods])
+    with torch.cuda.device(dev):
+        rc = L.mm_methods_host(ids, len(methods), A.data_ptr(), B.data_ptr(), cs, N, P, M, levels, row_blocks, ws_ptr,
+                               ws_len, s.cuda_stream)
+    _check(rc, "mm_methods_host")
     return outs
 
 

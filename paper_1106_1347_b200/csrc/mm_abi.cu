@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "dist_nccl.cuh"
 #include "gemm_tma.cuh"
+#include "host_pipeline.cuh"
 #include "kahan.cuh"
 #include "lines.cuh"
 #include "strassen.cuh"
@@ -351,6 +352,160 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
       return mm_winograd_scaled_fused(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
     default: return MM_ERR_ARG;
   }
+}
+
+// ---------------------------------------------------------------- host buffers (the paper's test program)
+static size_t host_ws_method(const int* methods, int32_t n, int64_t N, int64_t P, int64_t M, int32_t levels) {
+  size_t w = 0;
+  for (int i = 0; i < n; ++i) {
+    const size_t x = mm_workspace_size(methods[i], N, P, M, levels);
+    w = x > w ? x : w;
+  }
+  return w;
+}
+
+size_t mm_methods_host_workspace_size(const int* methods, int32_t n, int64_t N, int64_t P, int64_t M,
+                                      int32_t levels) {
+  if (!methods || n < 1 || N < 1 || P < 1 || M < 1 || !mul_ok(N, P) || !mul_ok(P, M) || !mul_ok(N, M)) return 0;
+  const size_t nc = n > 1 ? 2 : 1;
+  return mmk::align256(size_t(N) * size_t(P) * 8) + mmk::align256(size_t(P) * size_t(M) * 8) +
+         nc * mmk::align256(size_t(N) * size_t(M) * 8) + host_ws_method(methods, n, N, P, M, levels);
+}
+
+int mm_methods_host(const int* methods, int32_t n, const double* A_host, const double* B_host, double* const* C_host,
+                    int64_t N, int64_t P, int64_t M, int32_t levels, int32_t row_blocks, void* dev_ws, size_t ws_bytes,
+                    void* stream) {
+  mmk::NvtxRange nvtx("mm_methods_host");
+  if (!methods || n < 1 || !A_host || !B_host || !C_host || N < 1 || P < 1 || M < 1) return MM_ERR_ARG;
+  if (!mul_ok(N, P) || !mul_ok(P, M) || !mul_ok(N, M)) return MM_ERR_ARG;
+  for (int i = 0; i < n; ++i)
+    if (methods[i] < MM_NAIVE || methods[i] > MM_WINOGRAD_SCALED_FUSED || !C_host[i]) return MM_ERR_ARG;
+  if (!dev_ws || ws_bytes < mm_methods_host_workspace_size(methods, n, N, P, M, levels)) return MM_ERR_WORKSPACE;
+  int rc = check_device(nullptr);
+  if (rc) return rc;
+  mmk::HostStreams* hs = mmk::host_streams();
+  if (!hs) return MM_ERR_CUDA;
+  cudaStream_t st = S(stream), si = hs->in, so = hs->out;
+  char* w = static_cast<char*>(dev_ws);
+  double* dA = reinterpret_cast<double*>(w);
+  w += mmk::align256(size_t(N) * size_t(P) * 8);
+  double* dB = reinterpret_cast<double*>(w);
+  w += mmk::align256(size_t(P) * size_t(M) * 8);
+  double* dC[2];
+  dC[0] = reinterpret_cast<double*>(w);
+  w += mmk::align256(size_t(N) * size_t(M) * 8);
+  dC[1] = n > 1 ? reinterpret_cast<double*>(w) : dC[0];
+  if (n > 1) w += mmk::align256(size_t(N) * size_t(M) * 8);
+  void* wsm = w;
+  const size_t wsm_bytes = host_ws_method(methods, n, N, P, M, levels);
+
+  std::vector<cudaEvent_t> evs;  // every event of this call, destroyed at the end
+  auto event = [&](cudaStream_t on, cudaEvent_t* out) -> cudaError_t {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) return r;
+    evs.push_back(e);
+    *out = e;
+    return cudaEventRecord(e, on);
+  };
+  auto finish = [&](int code) {
+    cudaError_t e1 = cudaStreamSynchronize(so), e2 = cudaStreamSynchronize(st), e3 = cudaStreamSynchronize(si);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (code) return code;
+    return cuda_status(e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3));
+  };
+#define MMH_TRY(x)                                \
+  do {                                            \
+    cudaError_t _e = (x);                         \
+    if (_e != cudaSuccess) return finish(cuda_status(_e)); \
+  } while (0)
+#define MMH_RC(x)                       \
+  do {                                  \
+    int _r = (x);                       \
+    if (_r) return finish(_r);          \
+  } while (0)
+
+  cudaEvent_t e0;
+  MMH_TRY(event(st, &e0));  // the device buffers may be reused once prior work on `stream` is done
+  MMH_TRY(cudaStreamWaitEvent(si, e0, 0));
+  MMH_TRY(cudaStreamWaitEvent(so, e0, 0));
+  const int rb = row_blocks < 1 ? 1 : (row_blocks > N ? int(N) : row_blocks);
+  // ---- inputs: k-panels (first method NaivStandard) or B then row blocks of A
+  std::vector<int64_t> kb, ab;
+  std::vector<cudaEvent_t> ready;
+  if (methods[0] == MM_NAIVE && P >= 4) {
+    kb = mmk::host_growing_panels(P, rb);
+    for (size_t j = 0; j + 1 < kb.size(); ++j) {
+      const int64_t k0 = kb[j], k1 = kb[j + 1];
+      MMH_TRY(cudaMemcpy2DAsync(dA + k0, size_t(P) * 8, A_host + k0, size_t(P) * 8, size_t(k1 - k0) * 8, size_t(N),
+                                cudaMemcpyHostToDevice, si));
+      MMH_TRY(cudaMemcpyAsync(dB + k0 * M, B_host + k0 * M, size_t(k1 - k0) * size_t(M) * 8, cudaMemcpyHostToDevice,
+                              si));
+      cudaEvent_t e;
+      MMH_TRY(event(si, &e));
+      ready.push_back(e);
+    }
+  } else {
+    MMH_TRY(cudaMemcpyAsync(dB, B_host, size_t(P) * size_t(M) * 8, cudaMemcpyHostToDevice, si));
+    const int nb = mmk::host_row_local(methods[0]) ? rb : 1;
+    for (int b = 0; b <= nb; ++b) ab.push_back(N * b / nb);
+    for (int b = 0; b < nb; ++b) {
+      MMH_TRY(cudaMemcpyAsync(dA + ab[b] * P, A_host + ab[b] * P, size_t(ab[b + 1] - ab[b]) * size_t(P) * 8,
+                              cudaMemcpyHostToDevice, si));
+      cudaEvent_t e;
+      MMH_TRY(event(si, &e));
+      ready.push_back(e);
+    }
+  }
+  cudaEvent_t inputs_done = ready.back();
+  cudaEvent_t buf_free[2] = {nullptr, nullptr};
+  // ---- the methods
+  for (int i = 0; i < n; ++i) {
+    const int m = methods[i];
+    const int k = i % 2;
+    double* C = dC[k];
+    if (buf_free[k]) MMH_TRY(cudaStreamWaitEvent(st, buf_free[k], 0));  // its previous product has left
+    auto d2h = [&](int64_t lo, int64_t hi) -> cudaError_t {
+      cudaEvent_t e;
+      cudaError_t r = event(st, &e);
+      if (r == cudaSuccess) r = cudaStreamWaitEvent(so, e, 0);
+      if (r == cudaSuccess)
+        r = cudaMemcpyAsync(C_host[i] + lo * M, C + lo * M, size_t(hi - lo) * size_t(M) * 8, cudaMemcpyDeviceToHost,
+                            so);
+      return r;
+    };
+    const bool first = i == 0, last = i == n - 1;
+    if (first && !kb.empty()) {  // NaivStandard accumulating k-panels as they land
+      for (size_t j = 0; j + 1 < kb.size(); ++j) {
+        MMH_TRY(cudaStreamWaitEvent(st, ready[j], 0));
+        MMH_RC(mm_naive_ex(dA + kb[j], P, dB + kb[j] * M, M, C, M, N, kb[j + 1] - kb[j], M, j > 0 ? 1 : 0, stream));
+      }
+      MMH_TRY(d2h(0, N));
+    } else if (first && mmk::host_row_local(m) && ab.size() > 2) {  // row blocks as A lands
+      for (size_t b = 0; b + 1 < ab.size(); ++b) {
+        MMH_TRY(cudaStreamWaitEvent(st, ready[b], 0));
+        MMH_RC(mm_gemm(m, dA + ab[b] * P, dB, C + ab[b] * M, ab[b + 1] - ab[b], P, M, levels, wsm, wsm_bytes, nullptr,
+                       stream));
+        MMH_TRY(d2h(ab[b], ab[b + 1]));
+      }
+    } else if (last && mmk::host_row_local(m) && n > 1) {  // halving row blocks: a small last copy
+      MMH_TRY(cudaStreamWaitEvent(st, inputs_done, 0));
+      const std::vector<int64_t> tb = mmk::host_shrinking_rows(N, rb);
+      for (size_t b = 0; b + 1 < tb.size(); ++b) {
+        MMH_RC(mm_gemm(m, dA + tb[b] * P, dB, C + tb[b] * M, tb[b + 1] - tb[b], P, M, levels, wsm, wsm_bytes, nullptr,
+                       stream));
+        MMH_TRY(d2h(tb[b], tb[b + 1]));
+      }
+    } else {
+      MMH_TRY(cudaStreamWaitEvent(st, inputs_done, 0));
+      MMH_RC(mm_gemm(m, dA, dB, C, N, P, M, levels, wsm, wsm_bytes, nullptr, stream));
+      MMH_TRY(d2h(0, N));
+    }
+    MMH_TRY(event(so, &buf_free[k]));
+  }
+#undef MMH_TRY
+#undef MMH_RC
+  return finish(MM_OK);
 }
 
 // ---------------------------------------------------------------- multi-GPU row-block layer (K9)

@@ -25,3 +25,5 @@ def test_mmtest_c_client():
         assert name in rows, r.stdout
         assert 0.0 <= rows[name] < 1.875e-10, (name, rows[name])  # the n = 200 printed bands
     assert "C overlaps A or B" in r.stdout
+    # the host-buffer entry point (mm_methods_host) from C: Kahan's product is the device call's
+    assert "NaivKahan product bitwise the device call's: yes" in r.stdout, r.stdout

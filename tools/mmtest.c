@@ -140,6 +140,37 @@ int main(int argc, char** argv) {
     if (ws) CK(cudaFree(ws));
   }
   printf("+-----------------------------------------------------------------------+\n");
+  /* end to end from HOST memory through the ABI (mm_methods_host): the test program's six methods on
+   * page-locked copies of A and B, every product landing in host memory; Kahan's must equal N */
+  {
+    const int ms[] = {MM_NAIVE, MM_STRASSEN, MM_WINOGRAD_SCALED, MM_WINOGRAD, MM_STRASSEN_WINOGRAD, MM_KAHAN};
+    const int nm = (int)(sizeof(ms) / sizeof(ms[0]));
+    double *pA, *pB, *pC[6];
+    CK(cudaHostAlloc((void**)&pA, bytes, cudaHostAllocDefault));
+    CK(cudaHostAlloc((void**)&pB, bytes, cudaHostAllocDefault));
+    for (int i = 0; i < nm; i++) CK(cudaHostAlloc((void**)&pC[i], bytes, cudaHostAllocDefault));
+    memcpy(pA, hA, bytes);
+    memcpy(pB, hB, bytes);
+    const size_t hws = mm_methods_host_workspace_size(ms, nm, n, n, n, lv);
+    void* dws = NULL;
+    CK(cudaMalloc(&dws, hws));
+    int rc = mm_methods_host(ms, nm, pA, pB, pC, n, n, n, lv, 4, dws, hws, 0); /* warm-up */
+    CK(cudaEventRecord(e0, 0));
+    if (rc == MM_OK) rc = mm_methods_host(ms, nm, pA, pB, pC, n, n, n, lv, 4, dws, hws, 0);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms_e2e = 0.f;
+    CK(cudaEventElapsedTime(&ms_e2e, e0, e1));
+    const int same = rc == MM_OK && memcmp(pC[nm - 1], hN, bytes) == 0;
+    printf("end to end from host memory (mm_methods_host, %d methods, levels %d): %s, %.3f ms; "
+           "NaivKahan product bitwise the device call's: %s\n",
+           nm, lv, mm_status_string(rc), ms_e2e, same ? "yes" : "NO");
+    cudaFree(dws);
+    cudaFreeHost(pA);
+    cudaFreeHost(pB);
+    for (int i = 0; i < nm; i++) cudaFreeHost(pC[i]);
+    if (!same) return 4;
+  }
   /* the C ABI's error paths, from C */
   int bad = mm_naive(NULL, B, C, n, n, n, 0);
   int alias = mm_naive(A, B, A, n, n, n, 0);
