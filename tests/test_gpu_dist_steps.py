@@ -94,3 +94,28 @@ def test_odd_shapes_take_the_one_shot_path():
         assert torch.equal(C, getattr(mm, m)(dA, dB)), m
     C, kinds = _run_ranks("naive", dA, dB, 2, 4, 2)  # odd P: even k-panels, odd last panel
     assert d.OP_PANEL in kinds and torch.equal(C, mm.naive(dA, dB))
+
+
+def test_misaligned_shard_keeps_the_collectives():
+    # a rank whose A shard is only 8-byte aligned cannot take the TMA-fed panel kernels.
+    # The schedule (hence the collectives) does not depend on the shard; the rank's PANEL steps skip
+    # and the one-shot kernel runs at the last one -- bitwise the same rows.
+    N, P, M = 96, 256, 130
+    A, B = workload.custom(N, P, M, seed=21)
+    dB = torch.from_numpy(B).to(DEV)
+    flat = torch.empty(N * P + 1, dtype=torch.float64, device=DEV)
+    A8 = flat[1:].view(N, P)  # data_ptr % 16 == 8
+    A8.copy_(torch.from_numpy(A))
+    assert A8.data_ptr() % 16 == 8
+    for m in ("kahan", "winograd", "kahan_fused", "winograd_fused"):
+        ops = d.schedule(m, P, M, 2, 4)
+        assert any(o.op == d.OP_PANEL for o in ops)
+        ref = getattr(mm, m)(torch.from_numpy(A).to(DEV), dB)
+        nb = d.workspace_bytes(m, N, P, M, 2)
+        ctx = dict(method=m, A=A8, B=dB, out=torch.full((N, M), np.nan, dtype=torch.float64, device=DEV), levels=2,
+                   is_root=True, ws=torch.empty(max(nb, 1), dtype=torch.uint8, device=DEV) if nb else None)
+        for o in ops:
+            if o.op not in (d.OP_BCAST, d.OP_ALLREDUCE_NORMS, d.OP_RECORD, d.OP_WAIT):
+                d.gpu_step(o, ctx)
+        torch.cuda.synchronize()
+        assert torch.equal(ctx["out"], ref), m
