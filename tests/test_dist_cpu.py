@@ -249,3 +249,78 @@ def test_row_sharded_bitwise(shape):
     assert d.OP_PANEL in traces[("naive", 3, 2)]
     assert (d.OP_PANEL in traces[("winograd_scaled", 3, 2)]) == (P % 2 == 0 and M % 2 == 0)
     assert d.OP_FORM_B in traces[("strassen_winograd", 2, 2)]
+
+
+def test_schedule_invariants_random():
+    """Properties of mm_dist_schedule over random (method, P, M, levels, panels), checked by
+    simulating which rows of B have arrived at every compute op: each row is broadcast exactly once;
+    a compute op only reads rows whose broadcast it has waited for (PANEL / SCALE_B: its k-range;
+    FORM_B: its units' 2^span row ranges; YZ / FULL / LEAF_COMBINE / FORM_B_REST: all of B); every
+    RECORD precedes its WAIT; the norms are all-reduced before anything reads lambda; PANEL k-ranges
+    tile [0, P) in increasing order with the accumulate / keep-state flags of a first / last panel."""
+    import random
+
+    from paper_1106_1347_b200 import dist as d
+
+    rng = random.Random(11061347)
+    for _ in range(400):
+        m = rng.choice(METHODS)
+        P, M = rng.randint(1, 5000), rng.randint(1, 300)
+        lv = rng.choice((-1, 0, 1, 2, 3, 4, 5))
+        n = rng.choice((1, 2, 3, 4, 7, 8, 16, 64))
+        ops = d.schedule(m, P, M, lv, n)
+        sent = np.zeros(P, dtype=np.int64)
+        pending, recorded, waited = [], {}, set()
+        arrived = np.zeros(P, dtype=bool)
+        reduced = False
+        norms_done = False
+        panels = []
+        for o in ops:
+            if o.op == d.OP_BCAST:
+                sent[o.lo:o.hi] += 1
+                pending.append((o.lo, o.hi))
+            elif o.op == d.OP_ALLREDUCE_NORMS:
+                assert norms_done, "all-reduce before the local norms"
+                pending.append("norms")
+            elif o.op == d.OP_RECORD:
+                if o.stream == d.STREAM_COMM:
+                    recorded[o.index] = pending
+                    pending = []
+                else:
+                    recorded[o.index] = ["compute"]
+            elif o.op == d.OP_WAIT:
+                assert o.index in recorded, "wait before record"
+                if o.stream == d.STREAM_COMPUTE:
+                    for item in recorded[o.index]:
+                        if item == "norms":
+                            reduced = True
+                        elif item != "compute":
+                            arrived[item[0]:item[1]] = True
+                waited.add(o.index)
+            else:
+                if o.op == d.OP_NORMS:
+                    norms_done = True
+                    continue
+                if o.op in (d.OP_SCALE_A, d.OP_SCALE_B, d.OP_FULL) and m.startswith("winograd_scaled"):
+                    assert reduced, "lambda read before the norms were all-reduced"
+                if o.op in (d.OP_PANEL, d.OP_SCALE_B):
+                    assert arrived[o.lo:o.hi].all(), (m, o)
+                    if o.op == d.OP_PANEL:
+                        panels.append(o)
+                elif o.op == d.OP_FORM_B:
+                    span = FIRST_SPAN[lv]
+                    q = 2 << lv
+                    h = (-(-P // q) * q) >> span
+                    for r in range(1 << span):
+                        a, b = min(P, r * h + o.lo), min(P, r * h + o.hi)
+                        assert arrived[a:b].all(), (m, o)
+                elif o.op in (d.OP_YZ, d.OP_FULL, d.OP_LEAF_COMBINE, d.OP_FORM_B_REST):
+                    assert arrived.all(), (m, o)
+        assert (sent == 1).all(), (m, P, M, lv, n)
+        if panels:
+            assert panels[0].lo == 0 and panels[-1].hi == P
+            assert all(a.hi == b.lo for a, b in zip(panels, panels[1:]))
+            assert not panels[0].flags & d.EX_ACCUMULATE and all(p.flags & d.EX_ACCUMULATE for p in panels[1:])
+            assert not panels[-1].flags & d.EX_KEEP_STATE
+            assert all(p.flags & d.EX_KEEP_STATE for p in panels[:-1]) or m == "naive"
+            assert all(bool(p.flags & d.EX_FUSED) == m.endswith("_fused") for p in panels)
