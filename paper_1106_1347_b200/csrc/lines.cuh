@@ -69,7 +69,8 @@ struct LineJob {
   const double* init;            // LN_PAIRS, optional: per-line start values (a sum continued over a
                                  // later row panel of B -- the multi-GPU scaled Winograd, mm_dist_step)
   unsigned long long* out_max;   // LN_ABS: max over lines, as the bit pattern of a non-negative double
-  double* copy;                  // optional scaled copy (same shape and ld as X)
+  double* copy;                  // optional scaled copy (same shape as X, row pitch copy_ld)
+  int64_t copy_ld;
   int by_rows;
   int op;
   int scale_sel;                 // -1: unscaled; 0: x 2^lambda; 1: x 2^-lambda (lambda from norms)
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
       } else if (jb.copy) {  // coalesced write of the scaled tile: lane = column
         const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
         if (lane < kv)
-          for (int r = 0; r < lv; ++r) jb.copy[(l0 + r) * jb.ld + k0 + lane] = dmul(s, t[ln_rowoff(r, lane)]);
+          for (int r = 0; r < lv; ++r) jb.copy[(l0 + r) * jb.copy_ld + k0 + lane] = dmul(s, t[ln_rowoff(r, lane)]);
       }
     } else {
       // column lines: lane = column l0 + lane, tile row k = element k0 + k of the line
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(LN_LINES) line_kernel(const __grid_constant__ 
       } else if (jb.copy) {  // lane = column; rows of the panel are 256-byte coalesced stores
         const int64_t lv = jb.nlines - l0 < LN_LINES ? jb.nlines - l0 : LN_LINES;
         if (lane < lv)
-          for (int k = 0; k < kv; ++k) jb.copy[(k0 + k) * jb.ld + l0 + lane] = dmul(s, t[k * LN_LINES + lane]);
+          for (int k = 0; k < kv; ++k) jb.copy[(k0 + k) * jb.copy_ld + l0 + lane] = dmul(s, t[k * LN_LINES + lane]);
       }
     }
     if (++st == S) {
@@ -371,10 +372,10 @@ inline void ln_finish_job(LineJob& j, CUtensorMap* map, CUtensorMap* cmap, int t
       j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, LN_LINES, 16, true);
     else
       j.bulk = tma_encode_2d(map, j.X, rows, cols, j.ld, tk, LN_LINES, false);
-    // the copy has X's shape and pitch: the same box geometry stores the (in place scaled) tile
-    if (j.bulk && j.copy && j.scale_sel >= 0 && tma_ok(j.copy, j.ld))
-      j.cbulk = j.by_rows ? tma_encode_2d(cmap, j.copy, rows, cols, j.ld, LN_LINES, 16, true)
-                          : tma_encode_2d(cmap, j.copy, rows, cols, j.ld, tk, LN_LINES, false);
+    // the copy has X's shape: the same box geometry stores the (in place scaled) tile
+    if (j.bulk && j.copy && j.scale_sel >= 0 && tma_ok(j.copy, j.copy_ld))
+      j.cbulk = j.by_rows ? tma_encode_2d(cmap, j.copy, rows, cols, j.copy_ld, LN_LINES, 16, true)
+                          : tma_encode_2d(cmap, j.copy, rows, cols, j.copy_ld, tk, LN_LINES, false);
   }
 }
 
@@ -434,6 +435,7 @@ inline LineJob ln_job(const double* X, int64_t ld, int64_t nlines, int64_t len, 
   j.nlines = nlines;
   j.len = len;
   j.pair_end = 2 * (len / 2);
+  j.copy_ld = ld;
   j.by_rows = by_rows ? 1 : 0;
   j.op = op;
   j.scale_sel = -1;
@@ -467,7 +469,7 @@ inline cudaError_t launch_norm_inf(const double* X, int64_t rows, int64_t cols, 
 // As = 2^lambda A, Bs = 2^-lambda B, which are written in the same pass (lambda from norms).
 inline cudaError_t launch_yz(const double* A, const double* B, double* y, double* z, int64_t N, int64_t P, int64_t M,
                              double* As, double* Bs, const unsigned long long* norms, int* lam_out, double* scale_out,
-                             cudaStream_t st, bool fused = false) {
+                             cudaStream_t st, bool fused = false, int64_t as_ld = 0) {
   LineLaunch L{};
   L.njobs = 2;
   L.norms = norms;
@@ -484,6 +486,7 @@ inline cudaError_t launch_yz(const double* A, const double* B, double* y, double
   L.job[1].out = z;
   if (scaled) {
     L.job[0].copy = As;
+    if (as_ld) L.job[0].copy_ld = as_ld;  // an even pitch for odd P: the copy can feed the TMA kernel
     L.job[0].scale_sel = 0;
     L.job[1].copy = Bs;
     L.job[1].scale_sel = 1;
@@ -499,6 +502,7 @@ inline cudaError_t launch_yz(const double* A, const double* B, double* y, double
 // and the copies are bitwise those of launch_yz(..., As, Bs, ...).
 inline cudaError_t launch_scale_rows(const double* A, double* As, double* y, int64_t N, int64_t P,
                                      const unsigned long long* norms, cudaStream_t st, bool fused) {
+  // (the multi-GPU panel path: P even, so the copy keeps A's pitch)
   LineLaunch L{};
   L.njobs = 1;
   L.norms = norms;

@@ -76,7 +76,7 @@ size_t winograd_ws(int64_t N, int64_t M) {
 constexpr size_t kScaledHeader = 256;  // norms[2] (u64), scale[2] (double), lambda (int)
 // header | y | z | 2^lambda A | 2^-lambda B
 size_t scaled_ws(int64_t N, int64_t P, int64_t M) {
-  return kScaledHeader + winograd_ws(N, M) + mmk::align256(size_t(N) * size_t(P) * 8) +
+  return kScaledHeader + winograd_ws(N, M) + mmk::align256(size_t(N) * size_t(mmk::scaled_pitch(P)) * 8) +
          mmk::align256(size_t(P) * size_t(M) * 8);
 }
 
@@ -273,7 +273,8 @@ static int winograd_scaled_common(bool fused, const double* A, const double* B, 
   double* y = reinterpret_cast<double*>(ws + kScaledHeader);
   double* z = reinterpret_cast<double*>(ws + kScaledHeader + mmk::align256(size_t(N) * 8));
   double* As = reinterpret_cast<double*>(ws + kScaledHeader + winograd_ws(N, M));
-  double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(P) * 8));
+  double* Bs =
+      reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(mmk::scaled_pitch(P)) * 8));
   cudaStream_t st = S(stream);
   cudaError_t e = cudaSuccess;
   // K4 norms -> lambda + exact copies 2^lambda A, 2^-lambda B + their y, z -> pair sums.
@@ -617,7 +618,8 @@ int mm_dist_step(int method, const mm_dist_op* op, const double* A, const double
   double* ys = reinterpret_cast<double*>(sw + kScaledHeader);
   double* zs = reinterpret_cast<double*>(sw + kScaledHeader + mmk::align256(size_t(N) * 8));
   double* As = reinterpret_cast<double*>(sw + kScaledHeader + winograd_ws(N, M));
-  double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(P) * 8));
+  double* Bs =
+      reinterpret_cast<double*>(reinterpret_cast<char*>(As) + mmk::align256(size_t(N) * size_t(mmk::scaled_pitch(P)) * 8));
   // Winograd: y | z; Kahan: the carried err E
   double* y = reinterpret_cast<double*>(ws);
   double* z = reinterpret_cast<double*>(ws + mmk::align256(size_t(N) * 8));

@@ -37,6 +37,10 @@ struct SimtTmaArgs {
   // stores the running state (Kahan: err into E; Winograd: the raw pair sum, no epilogue)
   double* E;
   int flags;
+  // WinogradScaled with odd P on its even-pitch copies: the pair loop covers the P - 1 columns
+  // the maps describe (P here), the epilogue adds A[i][P] B[P][k] read at pitches lda / ldb
+  int odd;
+  int64_t lda, ldb;
 };
 constexpr int SIMT_EX_ACC = 1, SIMT_EX_KEEP = 2;
 
@@ -291,6 +295,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
       for (int e = 0; e < 2; ++e) {
         const int64_t cc = col + e;
         out[e] = cc >= a.M ? 0.0 : keep ? acc[i][2 * c + e] : dsub(dsub(acc[i][2 * c + e], yi), a.z[cc]);
+        if (!EX && a.odd && cc < a.M) {  // + A_{i,P} B_{P,k}, after -y -z
+          const double al = a.A[row * a.lda + a.P], bl = a.B[a.P * a.ldb + cc];
+          out[e] = FUSED ? __fma_rn(al, bl, out[e]) : dadd(out[e], dmul(al, bl));
+        }
       }  // (acc - y_i) - z_k
       if (CV == 2 && col + 1 < a.M) {
         *reinterpret_cast<double2*>(a.C + row * a.M + col) = make_double2(out[0], out[1]);
@@ -349,6 +357,27 @@ inline cudaError_t launch_winograd_pairs_tma(const double* A, const double* B, d
   if (!simt_tma_args<CF>(args, A, B, C, N, P, M)) return cudaErrorInvalidValue;
   args.y = y;
   args.z = z;
+  const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
+  const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
+  return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)
+            : launch_simt_tma_t_<winograd_tma_kernel<CF, 1, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st);
+}
+
+// WinogradScaled, odd P: the pair sums of the even-pitch copies As (pitch lda) and Bs (pitch ldb)
+// over their first P - 1 columns / rows, then (acc - y) - z + As[i][P-1] Bs[P-1][k] -- per entry the
+// cp.async kernel's operations in its order, so bitwise the same
+template <class CF, bool FUSED>
+inline cudaError_t launch_winograd_pairs_tma_odd(const double* As, int64_t lda, const double* Bs, int64_t ldb,
+                                                 double* C, const double* y, const double* z, int64_t N, int64_t P,
+                                                 int64_t M, cudaStream_t st) {
+  using LY = SimtTmaLayout<CF>;
+  SimtTmaArgs args{};
+  if (!simt_tma_args<CF>(args, As, Bs, C, N, P - 1, M, lda, ldb)) return cudaErrorInvalidValue;
+  args.y = y;
+  args.z = z;
+  args.odd = 1;
+  args.lda = lda;
+  args.ldb = ldb;
   const unsigned grid = unsigned(cdiv(M, CF::BN) * cdiv(N, CF::BM));
   const bool cv = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && M % 2 == 0;
   return cv ? launch_simt_tma_t_<winograd_tma_kernel<CF, 2, FUSED>, CF::THREADS, LY::SMEM>(args, grid, st)

@@ -194,6 +194,10 @@ inline cudaError_t launch_winograd(const double* A, const double* B, double* C, 
   return launch_winograd_pairs<CF, FUSED>(A, B, C, y, z, N, P, M, st, sms);
 }
 
+// row pitch reserved for the copy 2^lambda A in the WinogradScaled workspace: P, or P + 1 when P is
+// odd (a pitch a TMA tensor map can describe)
+inline int64_t scaled_pitch(int64_t P) { return P + (P & 1); }
+
 // WinogradScaled: norms (one launch, K4) -> lambda, exact copies 2^lambda A and
 // 2^-lambda B, and their y / z (one fused launch) -> pair sums on the copies.  C is not rescaled
 // (P:216).  Norms are device {||A||, ||B||} bit patterns: given (e.g. the distributed driver's
@@ -204,10 +208,19 @@ inline cudaError_t launch_winograd_scaled(const double* A, const double* B, doub
                                           int* lam, double* scale, double* y, double* z, double* As, double* Bs,
                                           cudaStream_t st, int sms = 148) {
   cudaError_t e = cudaSuccess;
+  // odd P: the copy of A gets the even pitch P + 1 (scaled_pitch), which a tensor map can
+  // describe, so the TMA-fed pair kernel runs with the odd term in its epilogue (c3: the cp.async
+  // kernel otherwise)
+  const bool odd_tma = (P & 1) && P > 1 && M % 2 == 0 && tma_ok(As, P + 1) && tma_ok(Bs, M) &&
+                       cdiv(N, WinogradTma::BM) * cdiv(M, WinogradTma::BN) >= 2 * int64_t(sms) && N <= INT32_MAX &&
+                       M <= INT32_MAX;
+  const int64_t lda = odd_tma ? P + 1 : P;  // As occupies N x scaled_pitch(P) doubles either way
   if (!given) e = launch_norms(A, N, P, B, P, M, norms, st);
-  if (e == cudaSuccess) e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st, FUSED);
-  if (e == cudaSuccess) e = launch_winograd_pairs<void, FUSED>(As, Bs, C, y, z, N, P, M, st, sms);
-  return e;
+  if (e == cudaSuccess)
+    e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st, FUSED, lda);
+  if (e != cudaSuccess) return e;
+  if (odd_tma) return launch_winograd_pairs_tma_odd<WinogradTma, FUSED>(As, lda, Bs, M, C, y, z, N, P, M, st);
+  return launch_winograd_pairs<void, FUSED>(As, Bs, C, y, z, N, P, M, st, sms);
 }
 
 }  // namespace mmk

@@ -465,3 +465,23 @@ def test_strassen_deep_levels_bitwise(levels):
         ref = oracle.strassen(v, A, B, levels=d, pad=pad, base=oracle.BASE_FMA)
         assert np.array_equal(C, ref), (name, levels)
     mm.release_workspace()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("shape", [(2048, 301, 1280), (1200, 1001, 2500), (2100, 3, 1300)])
+def test_scaled_odd_p_tma_copy(shape, fused):
+    """WinogradScaled with odd P gives its copy of 2^lambda A the even pitch P + 1, so the TMA-fed
+    pair kernel runs (>= 2 waves of 128 x 64 tiles) with the odd term A_{i,P} B_{P,k} in its
+    epilogue: bitwise the oracle, sampled entries + full first / last rows."""
+    N, P, M = shape
+    A, B = workload.custom(N, P, M, seed=P)
+    A = A * 1e5  # lambda != 0
+    f = mm.winograd_scaled_fused if fused else mm.winograd_scaled
+    C, lam = f(dev(A), dev(B), return_lambda=True)
+    C = host(C)
+    assert lam == oracle.lam(oracle.norm_inf(A), oracle.norm_inf(B)) != 0
+    idx = _sample(77, N, M, 2048) + [(0, j) for j in range(M)] + [(N - 1, j) for j in range(M)]
+    m = oracle.M_WINOGRAD_SCALED_FUSED if fused else oracle.M_WINOGRAD_SCALED
+    ref = oracle.entries(m, A, B, idx, lam)
+    got = np.array([C[i, j] for i, j in idx])
+    assert np.array_equal(got, ref), (shape, fused, np.abs(got - ref).max())
