@@ -12,6 +12,8 @@ with the counts the method's definition implies (n = 2048):
   K3 Winograd:     DMUL = n^2 n/2, DADD = 3 n^2 n/2 (+ 2 n^2 epilogue), DFMA = 0
   K3 Winograd fused (R22):     DFMA = n^2 n/2, DADD = 2 n^2 n/2 (+ 2 n^2)
   y/z line kernel:             DMUL = DADD = 2 n n/2 (or DFMA = 2 n n/2 fused)
+  Strassen-Winograd leaves:    DMMA ~ (7/8)^d n^3 / 256 (d = 2 batched K1; d = 3 the fused combination
+                               kernel, whose epilogue adds 0 DMUL / DFMA and a few DADD per output)
 """
 import csv
 import os
@@ -24,6 +26,8 @@ FP_METRICS = ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread
 
 def run():
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    # the fused S-W combination (NEXT-1) at 2048^3, d = 3 (below its default size threshold)
+    os.environ["MM_STRASSEN_FUSED_COMBINE"] = "1"
     import torch
 
     import paper_1106_1347_b200 as mm
@@ -34,6 +38,7 @@ def run():
     for name in ("naive", "kahan", "kahan_fused", "winograd", "winograd_fused"):
         getattr(mm, name)(A, B)
     mm.strassen_winograd(A, B, levels=2)
+    mm.strassen_winograd(A, B, levels=3)  # leaves in the fused combination kernel: (7/8)^3 of the DMMAs
     torch.cuda.synchronize()
 
 
