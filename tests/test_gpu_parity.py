@@ -485,3 +485,23 @@ def test_scaled_odd_p_tma_copy(shape, fused):
     ref = oracle.entries(m, A, B, idx, lam)
     got = np.array([C[i, j] for i, j in idx])
     assert np.array_equal(got, ref), (shape, fused, np.abs(got - ref).max())
+
+
+def test_methods_host_edge_cases():
+    """mm_methods_host through matmul / matmul_methods: pageable (not page-locked) host tensors, a
+    single method, a repeated method, shared output tensors, odd P, the paper's Strassen plan --
+    every product bitwise the device call's."""
+    A, B = workload.custom(301, 127, 259, seed=31)
+    dA, dB = dev(A), dev(B)
+    hA, hB = torch.from_numpy(A), torch.from_numpy(B)  # pageable
+    for m in ("naive", "kahan", "winograd", "winograd_scaled", "strassen_winograd"):
+        C = mm.matmul(hA, hB, m, levels=2)
+        assert np.array_equal(C.numpy(), host(run(m, dA, dB, 2))), m
+    outs = mm.matmul_methods(hA.pin_memory(), hB.pin_memory(), ["kahan", "naive", "kahan"], levels=2)
+    assert np.array_equal(outs["kahan"].numpy(), host(run("kahan", dA, dB, 2)))
+    shared = torch.empty((301, 259), dtype=torch.float64).pin_memory()
+    outs = mm.matmul_methods(hA.pin_memory(), hB.pin_memory(), ["naive", "winograd"], levels=2,
+                             outs={"naive": shared, "winograd": shared})
+    assert np.array_equal(shared.numpy(), host(run("winograd", dA, dB, 2)))  # the last product wins
+    C = mm.matmul(hA, hB, "strassen", levels=-1)
+    assert np.array_equal(C.numpy(), host(run("strassen", dA, dB, -1)))
