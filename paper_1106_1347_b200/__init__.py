@@ -154,6 +154,9 @@ def _workspace(nbytes: int, device, stream=None) -> Tuple[int, int]:
     key = (dev.index, s.cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
+        # drop the smaller buffer first: at c5 sizes the old and the new one need not fit together
+        _ws.pop(key, None)
+        del buf
         with torch.cuda.stream(s):
             buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         _ws[key] = buf

@@ -105,3 +105,28 @@ def test_dist_layer_host_errors():
     assert L.mm_dist_init(0, 1, None, 0) == -1
     assert L.mm_dist_workspace_size(3, 4, 5, 6, 0) >= L.mm_workspace_size(3, 4, 5, 6, 0) + 256
     assert b"NCCL" in L.mm_status_string(-5)
+
+
+def test_schedule_and_host_entry_errors():
+    """mm_dist_schedule / mm_dist_step / mm_methods_host reject bad arguments on the host."""
+    import ctypes
+
+    import paper_1106_1347_b200 as mm
+    from paper_1106_1347_b200 import dist as d
+
+    L = mm.lib()
+    ops = (d.DistOp * 4)()
+    assert L.mm_dist_schedule(99, 64, 64, 2, 2, ops, 4) == -1  # unknown method
+    assert L.mm_dist_schedule(0, 0, 64, 2, 2, ops, 4) == -1  # P < 1
+    assert L.mm_dist_schedule(4, 64, 64, 9, 2, ops, 4) == -1  # levels out of range
+    assert L.mm_dist_schedule(0, 8192, 8192, 2, 8, ops, 4) == -1  # the list does not fit
+    assert L.mm_dist_schedule(0, 8192, 8192, 2, 1, ops, 4) == 4  # one broadcast, record, wait, full
+    assert [o.op for o in ops] == [d.OP_BCAST, d.OP_RECORD, d.OP_WAIT, d.OP_FULL]
+    assert L.mm_dist_step(0, None, None, None, None, 1, 1, 1, 0, 0, None, 0, None) == -1
+    ids = (ctypes.c_int * 2)(0, 1)
+    assert L.mm_methods_host_workspace_size(None, 2, 4, 4, 4, 0) == 0
+    assert L.mm_methods_host_workspace_size(ids, 2, 4, 5, 6, 0) >= 8 * (4 * 5 + 5 * 6 + 2 * 4 * 6)
+    bad = (ctypes.c_int * 1)(42)
+    outs = (ctypes.c_void_p * 1)(1 << 20)
+    assert L.mm_methods_host(bad, 1, 1 << 20, 1 << 21, outs, 4, 4, 4, 0, 1, 1 << 22, 1 << 20, None) == -1
+    assert L.mm_methods_host(ids, 2, None, 1 << 21, outs, 4, 4, 4, 0, 1, 1 << 22, 1 << 20, None) == -1
