@@ -12,7 +12,6 @@ Bars (BASELINE.json north_star + DESIGN.md):
     (classical/Kahan/Winograd) or 1e-10 ||A|| ||B|| (Strassen variants, scaled Winograd);
   * integer-valued inputs (entries in [-8, 8]) are exact for every method.
 """
-import ctypes
 
 import numpy as np
 import pytest
