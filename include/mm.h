@@ -169,7 +169,10 @@ int mm_strassen_winograd(const double* A, const double* B, double* C, int64_t N,
 int mm_strassen_plan(int64_t N, int64_t P, int64_t M, int32_t levels, int32_t* depth_out, int64_t* Np_out,
                      int64_t* Pp_out, int64_t* Mp_out);
 
-/* Workspace bytes the given method needs (0 for MM_NAIVE and MM_KAHAN); 0 on bad arguments. */
+/* Workspace bytes the given method needs; 0 on bad arguments.  MM_NAIVE and MM_KAHAN[_FUSED] need
+ * none with even P; with odd P they report N (P + 1) doubles, which mm_gemm uses (when given) to copy
+ * A to an even row pitch so the TMA-fed kernels apply (a tiled TMA box cannot start on an 8-byte
+ * boundary) -- same result bit for bit; MM_WINOGRAD[_FUSED] likewise add that room to y | z. */
 size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels);
 
 /*

@@ -13,6 +13,7 @@
 #include "gemm_tma.cuh"
 #include "host_pipeline.cuh"
 #include "kahan.cuh"
+#include "repack.cuh"
 #include "lines.cuh"
 #include "strassen.cuh"
 #include "winograd.cuh"
@@ -73,6 +74,8 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 size_t winograd_ws(int64_t N, int64_t M) {
   return mmk::align256(size_t(N) * 8) + mmk::align256(size_t(M) * 8);
 }
+// odd P: room for A copied to the even pitch P + 1 (repack.cuh), used when the caller passes it
+size_t repack_ws(int64_t N, int64_t P) { return (P & 1) ? mmk::align256(size_t(N) * size_t(P + 1) * 8) : 0; }
 constexpr size_t kScaledHeader = 256;  // norms[2] (u64), scale[2] (double), lambda (int)
 // header | y | z | 2^lambda A | 2^-lambda B
 size_t scaled_ws(int64_t N, int64_t P, int64_t M) {
@@ -209,9 +212,9 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
   switch (method) {
     case MM_NAIVE:
     case MM_KAHAN:
-    case MM_KAHAN_FUSED: return 0;
+    case MM_KAHAN_FUSED: return repack_ws(N, P);
     case MM_WINOGRAD:
-    case MM_WINOGRAD_FUSED: return winograd_ws(N, M);
+    case MM_WINOGRAD_FUSED: return winograd_ws(N, M) + repack_ws(N, P);
     case MM_WINOGRAD_SCALED:
     case MM_WINOGRAD_SCALED_FUSED: return scaled_ws(N, P, M);
     case MM_STRASSEN:
@@ -222,6 +225,16 @@ size_t mm_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t le
     }
     default: return 0;
   }
+}
+
+// the repack path: odd P, a large enough grid of the TMA kernel's tiles (>= `waves` full waves at
+// 2 CTAs per SM), M even, a 16-byte aligned B and workspace room for the copy
+static bool repack_ok(const double* A, const double* B, int64_t N, int64_t P, int64_t M, size_t room, int bm, int bn,
+                      int waves, int sms) {
+  if (!(P & 1) || P < 3 || M % 2 || room < repack_ws(N, P) || !mmk::tma_ok(B, M)) return false;
+  if (N > INT32_MAX || P > INT32_MAX || M > INT32_MAX) return false;
+  (void)A;
+  return mmk::cdiv(N, int64_t(bm)) * mmk::cdiv(M, int64_t(bn)) >= int64_t(waves) * 2 * sms;
 }
 
 static int winograd_common(bool fused, const double* A, const double* B, double* C, int64_t N, int64_t P,
@@ -235,6 +248,18 @@ static int winograd_common(bool fused, const double* A, const double* B, double*
   if ((rc = check_device(&sms))) return rc;
   double* y = static_cast<double*>(workspace);
   double* z = reinterpret_cast<double*>(static_cast<char*>(workspace) + mmk::align256(size_t(N) * 8));
+  double* Ar = reinterpret_cast<double*>(static_cast<char*>(workspace) + winograd_ws(N, M));
+  if (repack_ok(A, B, N, P, M, ws_bytes - winograd_ws(N, M), mmk::WinogradTma::BM, mmk::WinogradTma::BN, 2, sms)) {
+    // odd P: A at pitch P + 1, then the TMA-fed pair kernel with the odd term in its epilogue
+    cudaStream_t st = S(stream);
+    cudaError_t e = mmk::launch_repack_rows(A, P, Ar, P + 1, N, P, sms, st);
+    if (e == cudaSuccess)
+      e = mmk::launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, st, fused);
+    if (e == cudaSuccess)
+      e = fused ? mmk::launch_winograd_pairs_tma_odd<mmk::WinogradTma, true>(Ar, P + 1, B, M, C, y, z, N, P, M, st)
+                : mmk::launch_winograd_pairs_tma_odd<mmk::WinogradTma, false>(Ar, P + 1, B, M, C, y, z, N, P, M, st);
+    return cuda_status(e);
+  }
   return cuda_status(fused ? mmk::launch_winograd<void, true>(A, B, C, y, z, N, P, M, S(stream), sms)
                            : mmk::launch_winograd<void, false>(A, B, C, y, z, N, P, M, S(stream), sms));
 }
@@ -338,16 +363,52 @@ int mm_strassen_winograd(const double* A, const double* B, double* C, int64_t N,
   return strassen_common(mmk::SV_WINOGRAD, A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
 }
 
+// NaivStandard / NaivKahan with odd P and the caller's workspace: A copied to the even pitch P + 1
+// (repack.cuh), then the TMA-fed kernels on the copy -- bitwise the direct calls' results
+static int gemm_repacked(int method, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  int rc = check_abc(A, B, C, N, P, M);
+  if (rc) return rc;
+  int sms = 148;
+  if ((rc = check_device(&sms))) return rc;
+  double* Ar = static_cast<double*>(workspace);
+  if (overlaps(Ar, N * (P + 1), A, N * P) || overlaps(Ar, N * (P + 1), B, P * M) ||
+      overlaps(Ar, N * (P + 1), C, N * M))
+    return MM_ERR_ALIAS;
+  const bool naive = method == MM_NAIVE;
+  const bool ok = naive ? repack_ok(A, B, N, P, M, ws_bytes, mmk::GemmTma::BM, mmk::GemmTma::BN, 2, sms)
+                        : repack_ok(A, B, N, P, M, ws_bytes, mmk::KahanTma::BM, mmk::KahanTma::BN, 2, sms);
+  if (!ok)
+    return naive ? mm_naive(A, B, C, N, P, M, stream)
+           : method == MM_KAHAN ? mm_kahan(A, B, C, N, P, M, stream)
+                                : mm_kahan_fused(A, B, C, N, P, M, stream);
+  cudaStream_t st = S(stream);
+  cudaError_t e = mmk::launch_repack_rows(A, P, Ar, P + 1, N, P, sms, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (naive) {
+    mmk::GemmProblem pr{Ar, B, C, N, P, M, P + 1, M, M, 0, 0, 0, 1};
+    return cuda_status(mmk::launch_dgemm(pr, st, sms));
+  }
+  return cuda_status(method == MM_KAHAN
+                         ? mmk::launch_kahan_tma_ex<mmk::KahanTma, false>(Ar, P + 1, B, M, C, nullptr, N, P, M, 0, st)
+                         : mmk::launch_kahan_tma_ex<mmk::KahanTma, true>(Ar, P + 1, B, M, C, nullptr, N, P, M, 0, st));
+}
+
 int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, int64_t P, int64_t M,
             int32_t levels, void* workspace, size_t ws_bytes, int32_t* lambda_out, void* stream) {
   switch (method) {
-    case MM_NAIVE: return mm_naive(A, B, C, N, P, M, stream);
-    case MM_KAHAN: return mm_kahan(A, B, C, N, P, M, stream);
+    case MM_NAIVE:
+    case MM_KAHAN:
+    case MM_KAHAN_FUSED:
+      if (workspace && (P & 1) && ws_bytes >= repack_ws(N, P)) return gemm_repacked(method, A, B, C, N, P, M, workspace,
+                                                                                    ws_bytes, stream);
+      return method == MM_NAIVE ? mm_naive(A, B, C, N, P, M, stream)
+             : method == MM_KAHAN ? mm_kahan(A, B, C, N, P, M, stream)
+                                  : mm_kahan_fused(A, B, C, N, P, M, stream);
     case MM_WINOGRAD: return mm_winograd(A, B, C, N, P, M, workspace, ws_bytes, stream);
     case MM_WINOGRAD_SCALED: return mm_winograd_scaled(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
     case MM_STRASSEN: return mm_strassen(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
     case MM_STRASSEN_WINOGRAD: return mm_strassen_winograd(A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
-    case MM_KAHAN_FUSED: return mm_kahan_fused(A, B, C, N, P, M, stream);
     case MM_WINOGRAD_FUSED: return mm_winograd_fused(A, B, C, N, P, M, workspace, ws_bytes, stream);
     case MM_WINOGRAD_SCALED_FUSED:
       return mm_winograd_scaled_fused(A, B, C, N, P, M, workspace, ws_bytes, lambda_out, stream);
