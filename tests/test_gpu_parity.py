@@ -504,3 +504,17 @@ def test_methods_host_edge_cases():
     assert np.array_equal(shared.numpy(), host(run("winograd", dA, dB, 2)))  # the last product wins
     C = mm.matmul(hA, hB, "strassen", levels=-1)
     assert np.array_equal(C.numpy(), host(run("strassen", dA, dB, -1)))
+
+
+def test_norm_inf_nan_and_inf():
+    """include/mm.h: a NaN row sum makes norm_inf NaN (the warp max would otherwise drop it); an
+    infinite row sum gives +inf.  (The paper's methods are defined on finite doubles, reading R24.)"""
+    for rows, cols in ((5, 7), (64, 40), (3000, 33)):
+        X = workload.custom(rows, cols, 1, rows + cols)[0]
+        for r in (0, rows // 2, rows - 1):
+            Y = X.copy()
+            Y[r, cols // 2] = np.nan
+            assert np.isnan(mm.norm_inf(dev(Y)).item()), (rows, cols, r)
+            Y[r, cols // 2] = -np.inf
+            assert mm.norm_inf(dev(Y)).item() == np.inf, (rows, cols, r)
+        assert mm.norm_inf(dev(X)).item() == oracle.norm_inf(X)

@@ -20,6 +20,11 @@ rm -f gpurun_out/ncu/full_naive.ncu-rep gpurun_out/ncu/full_winograd.ncu-rep
 timeout 900 python tools/paper_experiment.py --sizes 200,400,800,1600,3200,4096,8192 --json gpurun_out/paper_experiment.jsonl > gpurun_out/paper_experiment.txt 2>&1; echo paper rc=$?
 ./tools/mmtest -O 800 -R 10 > gpurun_out/mmtest.txt 2>&1; echo mmtest rc=$?
 timeout 900 python tools/table_bench.py --reps 5 > gpurun_out/table.jsonl 2> gpurun_out/table.err; echo table rc=$?
+# kernel-only (ncu) times per method call at c2 / c3
+python tools/kernel_times.py run --configs c2,c3 --manifest gpurun_out/kt_manifest.json > /dev/null 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/kt.csv \
+    python tools/kernel_times.py run --configs c2,c3 --manifest gpurun_out/kt_manifest.json > /dev/null 2>&1 && \
+python tools/kernel_times.py parse gpurun_out/kt.csv gpurun_out/kt_manifest.json > gpurun_out/kernel_times.jsonl; echo kt rc=$?
 # per-rank schedule timing at the c4 shard shapes (modelled E_g) and BASELINE.json's c5 config on one GPU
 timeout 900 python tools/shard_model.py --out gpurun_out/shard_model_c4.jsonl > gpurun_out/shard_model.log 2>&1; echo shard rc=$?
 timeout 1200 python bench.py --config c5 --methods naive,strassen_winograd --levels 2 --steps 3 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5 rc=$?
