@@ -256,8 +256,8 @@ static int winograd_common(bool fused, const double* A, const double* B, double*
     if (e == cudaSuccess)
       e = mmk::launch_yz(A, B, y, z, N, P, M, nullptr, nullptr, nullptr, nullptr, nullptr, st, fused);
     if (e == cudaSuccess)
-      e = fused ? mmk::launch_winograd_pairs_tma_odd<mmk::WinogradTma, true>(Ar, P + 1, B, M, C, y, z, N, P, M, st)
-                : mmk::launch_winograd_pairs_tma_odd<mmk::WinogradTma, false>(Ar, P + 1, B, M, C, y, z, N, P, M, st);
+      e = fused ? mmk::launch_winograd_pairs_tma_odd_auto<true>(Ar, P + 1, B, M, C, y, z, N, P, M, st, sms)
+                : mmk::launch_winograd_pairs_tma_odd_auto<false>(Ar, P + 1, B, M, C, y, z, N, P, M, st, sms);
     return cuda_status(e);
   }
   return cuda_status(fused ? mmk::launch_winograd<void, true>(A, B, C, y, z, N, P, M, S(stream), sms)

@@ -37,6 +37,23 @@ using Winograd96 = SimtCfg<96, 64, 6, 8, 2, 3>;
 // TMA-fed main loop (simt_tma.cuh) for 16-byte aligned operands with P, M even: 32-deep k tiles,
 // double-buffered -- 65.1 vs 65.6 ms (16-deep, 4 stages) at 8192^3
 using WinogradTma = SimtCfg<128, 64, 8, 8, 2, 2, 32>;
+// ... and a finer tile grid for shapes whose last wave of 128 x 64 tiles is mostly empty (c3: 5.08
+// waves; 96 x 64 at 3 CTAs per SM: 4.55), 2.5% slower per tile at 8192^3 (66.7 vs 65.1 ms)
+using WinogradTma96 = SimtCfg<96, 64, 6, 8, 3, 3, 16>;
+
+// odd P on even-pitch copies (repack.cuh / WinogradScaled's 2^lambda A): the TMA pair kernel with
+// the odd term in its epilogue, on the tile grid that fills its last wave better
+template <bool FUSED>
+inline cudaError_t launch_winograd_pairs_tma_odd_auto(const double* As, int64_t lda, const double* Bs, int64_t ldb,
+                                                      double* C, const double* y, const double* z, int64_t N,
+                                                      int64_t P, int64_t M, cudaStream_t st, int sms) {
+  const int64_t t128 = cdiv(N, WinogradTma::BM) * cdiv(M, WinogradTma::BN);
+  const int64_t t96 = cdiv(N, WinogradTma96::BM) * cdiv(M, WinogradTma96::BN);
+  const double f128 = double(t128) / double(cdiv(t128, 2 * int64_t(sms)) * 2 * sms);
+  const double f96 = 0.975 * double(t96) / double(cdiv(t96, 3 * int64_t(sms)) * 3 * sms);
+  if (f96 > f128) return launch_winograd_pairs_tma_odd<WinogradTma96, FUSED>(As, lda, Bs, ldb, C, y, z, N, P, M, st);
+  return launch_winograd_pairs_tma_odd<WinogradTma, FUSED>(As, lda, Bs, ldb, C, y, z, N, P, M, st);
+}
 
 // The tiles are loaded with kend = 2*gamma: columns/rows >= 2*gamma are zero-filled, so the
 // odd column never enters acc.  A zero-filled pair adds (0+0)(0+0) = +0 to acc, which leaves
@@ -219,7 +236,7 @@ inline cudaError_t launch_winograd_scaled(const double* A, const double* B, doub
   if (e == cudaSuccess)
     e = launch_yz(A, B, y, z, N, P, M, As, Bs, given ? given : norms, lam, scale, st, FUSED, lda);
   if (e != cudaSuccess) return e;
-  if (odd_tma) return launch_winograd_pairs_tma_odd<WinogradTma, FUSED>(As, lda, Bs, M, C, y, z, N, P, M, st);
+  if (odd_tma) return launch_winograd_pairs_tma_odd_auto<FUSED>(As, lda, Bs, M, C, y, z, N, P, M, st, sms);
   return launch_winograd_pairs<void, FUSED>(As, Bs, C, y, z, N, P, M, st, sms);
 }
 
