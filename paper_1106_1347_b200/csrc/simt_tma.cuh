@@ -22,7 +22,19 @@
 #include "simt_tile.cuh"
 #include "tma.cuh"
 
+#ifndef MMK_WINO_SCHED  // inner-loop order of K3 (tools/tune/simt_tune.cu compares them)
+#define MMK_WINO_SCHED 0
+#endif
+#ifndef MMK_KAHAN_UNROLL
+#define MMK_KAHAN_UNROLL 4
+#endif
+#ifndef MMK_WINO_UNROLL
+#define MMK_WINO_UNROLL 8
+#endif
+
 namespace mmk {
+
+constexpr int kWinoUnroll = MMK_WINO_UNROLL, kKahanUnroll = MMK_KAHAN_UNROLL;
 
 struct SimtTmaArgs {
   CUtensorMap mapA, mapB;
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) kahan_tma_kernel(const 
     const double* Bs = pp.Bs_base + s * LY::B_TILE;
     const int64_t k0 = int64_t(kt) * CF::BK;
     if (k0 + CF::BK <= a.P) {
-#pragma unroll 4
+#pragma unroll kKahanUnroll
       for (int kk = 0; kk < CF::BK; ++kk) step(As, Bs, kk);
     } else {
       const int kmax = int(a.P - k0);  // stop exactly at P
@@ -260,7 +272,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
     // (acc starts at +0 and can never become -0), so the last tile needs no guard
     // per pair: B's TN column pairs stay in registers, A's pair of row i is read just before its
     // TN entries (64.70 vs 65.02 ms with all of A's pairs loaded up front; winograd_sched.log)
-#pragma unroll 2
+    // 8 pairs per unrolled body on the 2-CTA tiles: 63.9 vs 64.7 ms at 8192^3 with 2
+    // (tools/tune/simt_tune.cu x, profiles/r02/winograd_unroll.log); the 3-CTA tiles keep 2
+    constexpr int UNR = CF::MINB >= 3 ? 2 : kWinoUnroll;
+#pragma unroll UNR
     for (int jp = 0; jp < CF::BK / 2; ++jp) {
       double b0[TN], b1[TN];
 #pragma unroll
@@ -272,12 +287,57 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
         b1[2 * c] = w.x;
         b1[2 * c + 1] = w.y;
       }
+#if MMK_WINO_SCHED == 1
+      // per row: the 2 TN sums first, then the TN products, then the TN accumulations
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
+        double s1[TN], s2[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) s1[j] = dadd(v.x, b1[j]);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) s2[j] = dadd(v.y, b0[j]);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          if (FUSED) acc[i][j] = __fma_rn(s1[j], s2[j], acc[i][j]);
+          else s1[j] = dmul(s1[j], s2[j]);
+        }
+        if (!FUSED) {
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = dadd(acc[i][j], s1[j]);
+        }
+      }
+#elif MMK_WINO_SCHED == 2
+      // two rows interleaved: row i's products wait on sums issued a row-pair earlier
+#pragma unroll
+      for (int i = 0; i < TM; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
+        const double2 w = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i + 1), 2 * jp));
+        double s1[2][TN], s2[2][TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          s1[0][j] = dadd(v.x, b1[j]);
+          s1[1][j] = dadd(w.x, b1[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          s2[0][j] = dadd(v.y, b0[j]);
+          s2[1][j] = dadd(w.y, b0[j]);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i + r][j] = FUSED ? __fma_rn(s1[r][j], s2[r][j], acc[i + r][j])
+                                                              : dadd(acc[i + r][j], dmul(s1[r][j], s2[r][j]));
+      }
+#else
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const double2 v = *reinterpret_cast<const double2*>(As + sw_a<CF>(simt_row<CF>(ty, i), 2 * jp));
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = wino_pair<FUSED>(acc[i][j], v.x, v.y, b0[j], b1[j]);
       }
+#endif
     }
   }
 

@@ -140,7 +140,7 @@ int main(int argc, char** argv) {
   const bool wino_only = argc > 1 && argv[1][0] == 'w';
   const bool kahan_only = argc > 1 && argv[1][0] == 'k';
   Ctx c;
-  c.n = argc > 1 && !wino_only && !kahan_only ? atoll(argv[1]) : 8192;
+  c.n = argc > 1 && !wino_only && !kahan_only && argv[1][0] != 'x' && argv[1][0] != 'y' ? atoll(argv[1]) : 8192;
   c.reps = argc > 2 ? atoi(argv[2]) : 2;
   cudaMalloc(&c.A, c.n * c.n * 8);
   cudaMalloc(&c.B, c.n * c.n * 8);
@@ -183,6 +183,17 @@ int main(int argc, char** argv) {
     kahan_tma<SimtCfg<48, 64, 3, 8, 2, 3, 32>>("tma_48x64_t3x8_s2_3cta_bk32", c);
     kahan_tma<SimtCfg<64, 64, 4, 8, 6, 2, 16>>("tma_64x64_s6_2cta_bk16", c);
     kahan_tma<SimtCfg<64, 64, 4, 8, 5, 2, 16>>("tma_64x64_s5_2cta_bk16", c);
+    return 0;
+  }
+  if (argc > 1 && argv[1][0] == 'x') {  // the production K3 configuration only (schedule variants)
+    wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
+    wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_2cta_bk32", c);
+    wino_tma<SimtCfg<128, 64, 8, 8, 3, 2, 32>>("tma_128x64_s3_2cta_bk32", c);
+    return 0;
+  }
+  if (argc > 1 && argv[1][0] == 'y') {  // the production K2 configuration only (unroll variants)
+    kahan<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("cpasync_64x64_s2_bk32", c, true);
+    kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_s3_2cta_bk32", c);
     return 0;
   }
   if (wino_only) {  // K3 configurations only
