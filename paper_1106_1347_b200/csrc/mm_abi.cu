@@ -778,8 +778,10 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
           grouped = true;
         }
         double* Bp = B + o.lo * M;
-        if (api->Broadcast(Bp, Bp, size_t(o.hi - o.lo) * size_t(M), ncclFloat64, root, ds.comm, cs) != ncclSuccess)
+        if (api->Broadcast(Bp, Bp, size_t(o.hi - o.lo) * size_t(M), ncclFloat64, root, ds.comm, cs) != ncclSuccess) {
+          if (grouped) api->GroupEnd();  // leave no NCCL group open behind the error
           return MM_ERR_NCCL;
+        }
         if (grouped && !more) {
           if (api->GroupEnd() != ncclSuccess) return MM_ERR_NCCL;
           grouped = false;
