@@ -309,6 +309,13 @@ int mm_winograd_scaled_fused(const double* A, const double* B, double* C, int64_
 #define MM_OP_FORM_B_REST 12 /* Strassen: the remaining B-side passes */
 #define MM_OP_LEAF_COMBINE 13 /* Strassen: the batched leaf products and the combination passes */
 #define MM_OP_FULL 14        /* the one-GPU method on the shard (B complete) */
+/* the alternative partition of mm_s7_schedule (below) */
+#define MM_OP_BCAST_A 15     /* comm: broadcast rows [lo, hi) of A from the root */
+#define MM_OP_S7_FORM 16     /* the level-1 operands of product `index` (0..6 = H_1..H_7) */
+#define MM_OP_S7_PRODUCT 17  /* H_{index+1} = their product, levels - 1 further levels, into slot index */
+#define MM_OP_SEND_H 18      /* comm: send H slot `index` to rank lo */
+#define MM_OP_RECV_H 19      /* comm: receive H slot `index` from rank lo */
+#define MM_OP_S7_COMBINE 20  /* C from the seven H slots (the level-0 combination, P:279-282 / P:307-311) */
 #define MM_STREAM_COMPUTE 0
 #define MM_STREAM_COMM 1
 typedef struct {
@@ -329,6 +336,41 @@ int mm_dist_schedule(int method, int64_t P, int64_t M, int32_t levels, int32_t p
 int mm_dist_step(int method, const mm_dist_op* op, const double* A_shard, const double* B, double* C_shard,
                  int64_t N_local, int64_t P, int64_t M, int32_t levels, int32_t is_root, void* workspace,
                  size_t ws_bytes, void* stream);
+
+/*
+ * Alternative partition: Strassen's seven top-level products (P:270-277 /
+ * P:299-306) spread over the ranks -- product p (0..6, H_{p+1}) on rank p % world.  Not the
+ * default (DESIGN.md section 7 compares it with the row blocks).  Every rank receives A and B
+ * (broadcasts from the root), forms the level-1 operands of its products from the zero-embedded
+ * quadrants (the one-GPU formation's per-element operations), multiplies them with levels - 1
+ * further levels (the one-GPU recursion on that node), and sends each H to the root, which forms
+ * C by the level-0 combination.  The root's C is therefore bitwise the one-GPU mm_strassen /
+ * mm_strassen_winograd(levels) product.  method: MM_STRASSEN or MM_STRASSEN_WINOGRAD; levels >= 1
+ * (the GPU plan, reading R10).
+ *
+ * mm_s7_schedule -- the op list of `rank` (HOST array `ops` of `cap` entries, 64 always suffice;
+ *   returns the count or MM_ERR_ARG): MM_OP_BCAST_A / MM_OP_BCAST (every rank), RECORD / WAIT,
+ *   MM_OP_S7_FORM + MM_OP_S7_PRODUCT per owned product, MM_OP_SEND_H (owner -> root) /
+ *   MM_OP_RECV_H (root), MM_OP_S7_COMBINE (root).  A function of (method, N, P, M, levels, world,
+ *   rank, root) only; pure host function.  Consecutive SEND_H / RECV_H ops form one NCCL group.
+ * mm_s7_workspace_size -- DEVICE workspace bytes of one rank (0 on bad arguments).  Layout, for
+ *   h = (Np/2)(Mp/2) with (Np, Pp, Mp) = mm_strassen_plan(N, P, M, levels): seven contiguous H
+ *   slots of h doubles at offset 0 (slot p = H_{p+1}, dense (Np/2) x (Mp/2)), then the two level-1
+ *   operands and the workspace of the levels - 1 sub-product.  Executors move slot p with SEND_H /
+ *   RECV_H.
+ * mm_s7_step -- run ONE compute op of an mm_s7_schedule on `stream`: A (N x P) and B (P x M)
+ *   DEVICE buffers holding the root's data, C (N x M, DEVICE) used by MM_OP_S7_COMBINE only.
+ * mm_dist_strassen7 -- the NCCL executor of that schedule on the communicator of mm_dist_init: A
+ *   and B DEVICE buffers on every rank (the root's content broadcast into them in place), C on the
+ *   root (may be NULL elsewhere).  Stream-ordered and asynchronous like mm_dist_gemm.
+ */
+int mm_s7_schedule(int method, int64_t N, int64_t P, int64_t M, int32_t levels, int32_t world, int32_t rank,
+                   int32_t root, mm_dist_op* ops, int32_t cap);
+size_t mm_s7_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels);
+int mm_s7_step(int method, const mm_dist_op* op, const double* A, const double* B, double* C, int64_t N, int64_t P,
+               int64_t M, int32_t levels, void* workspace, size_t ws_bytes, void* stream);
+int mm_dist_strassen7(int method, double* A, double* B, double* C, int64_t N, int64_t P, int64_t M, int32_t root,
+                      int32_t levels, void* workspace, size_t ws_bytes, void* stream);
 
 /*
  * mm_launch_count -- number of kernels this library has launched in this process (a

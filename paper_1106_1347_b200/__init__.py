@@ -45,7 +45,8 @@ EXPORTS = ("mm_version", "mm_status_string", "mm_naive", "mm_kahan", "mm_winogra
            "mm_lambda", "mm_winograd_scaled_norms", "mm_launch_count", "mm_kahan_fused", "mm_winograd_fused",
            "mm_winograd_scaled_fused", "mm_naive_ex", "mm_dist_get_unique_id", "mm_dist_init",
            "mm_dist_workspace_size", "mm_dist_gemm", "mm_dist_finalize", "mm_kahan_ex", "mm_winograd_ex",
-           "mm_winograd_yz", "mm_dist_schedule", "mm_dist_step", "mm_methods_host", "mm_methods_host_workspace_size")
+           "mm_winograd_yz", "mm_dist_schedule", "mm_dist_step", "mm_methods_host", "mm_methods_host_workspace_size",
+           "mm_s7_schedule", "mm_s7_workspace_size", "mm_s7_step", "mm_dist_strassen7")
 MM_EX_ACCUMULATE, MM_EX_KEEP_STATE, MM_EX_FUSED = 1, 2, 4
 
 
@@ -84,6 +85,11 @@ def lib() -> ctypes.CDLL:
         L.mm_methods_host_workspace_size.restype = sz
         L.mm_methods_host.argtypes = [vp, i32, dp, dp, vp, i64, i64, i64, i32, i32, vp, sz, vp]
         L.mm_dist_step.argtypes = [ctypes.c_int, vp, dp, dp, dp, i64, i64, i64, i32, i32, vp, sz, vp]
+        L.mm_s7_schedule.argtypes = [ctypes.c_int, i64, i64, i64, i32, i32, i32, i32, vp, i32]
+        L.mm_s7_workspace_size.argtypes = [ctypes.c_int, i64, i64, i64, i32]
+        L.mm_s7_workspace_size.restype = sz
+        L.mm_s7_step.argtypes = [ctypes.c_int, vp, dp, dp, dp, i64, i64, i64, i32, vp, sz, vp]
+        L.mm_dist_strassen7.argtypes = [ctypes.c_int, dp, dp, dp, i64, i64, i64, i32, i32, vp, sz, vp]
         for n in ("mm_winograd", "mm_winograd_fused"):
             getattr(L, n).argtypes = [dp, dp, dp, i64, i64, i64, vp, sz, vp]
         for n in ("mm_winograd_scaled", "mm_winograd_scaled_fused"):

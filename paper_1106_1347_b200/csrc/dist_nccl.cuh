@@ -45,6 +45,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 inline NcclApi* nccl_api() {
@@ -64,8 +66,10 @@ inline NcclApi* nccl_api() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
     if (api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce && api.GroupStart &&
-        api.GroupEnd)
+        api.GroupEnd && api.Send && api.Recv)
       api.handle = h;
   });
   return api.handle ? &api : nullptr;
@@ -206,6 +210,43 @@ inline int build_dist_schedule(int method, int64_t P, int64_t M, int32_t levels,
     if (scaled) L.add(MM_OP_SCALE_B, MM_STREAM_COMPUTE, i, i > 0 ? MM_EX_ACCUMULATE : 0, kb[i], kb[i + 1]);
     if (wino && last) L.add(MM_OP_YZ, MM_STREAM_COMPUTE, i, fused, 0, P);
     L.add(MM_OP_PANEL, MM_STREAM_COMPUTE, i, fl, kb[i], kb[i + 1]);
+  }
+  return L.ok ? L.n : -1;
+}
+
+// ---- the alternative partition: Strassen's seven top-level products on the
+// ranks, product p (H_{p+1}) on rank p % world; A and B broadcast, each H sent to the root, which
+// combines.  Events: 0 = A and B arrived, 1 + p = product p done, 8 = every H at the root.
+constexpr int kS7EvInputs = 0, kS7EvGathered = 8;
+
+inline int s7_owner(int p, int world) { return p % world; }
+
+inline int build_s7_schedule(int method, int64_t N, int64_t P, int64_t M, int32_t levels, int32_t world, int32_t rank,
+                             int32_t root, mm_dist_op* ops, int cap) {
+  if (!ops || cap < 1 || N < 1 || P < 1 || M < 1 || levels < 1 || levels > 8) return -1;
+  if (method != MM_STRASSEN && method != MM_STRASSEN_WINOGRAD) return -1;
+  if (world < 1 || rank < 0 || rank >= world || root < 0 || root >= world) return -1;
+  OpList L{ops, cap, 0, true};
+  L.add(MM_OP_BCAST_A, MM_STREAM_COMM, 0, 0, 0, N);
+  L.add(MM_OP_BCAST, MM_STREAM_COMM, 0, 0, 0, P);
+  L.record(MM_STREAM_COMM, kS7EvInputs);
+  L.wait(MM_STREAM_COMPUTE, kS7EvInputs);
+  for (int p = 0; p < 7; ++p) {
+    if (s7_owner(p, world) != rank) continue;
+    L.add(MM_OP_S7_FORM, MM_STREAM_COMPUTE, p, 0, 0, 0);
+    L.add(MM_OP_S7_PRODUCT, MM_STREAM_COMPUTE, p, 0, 0, 0);
+    if (rank != root) {
+      L.record(MM_STREAM_COMPUTE, 1 + p);
+      L.wait(MM_STREAM_COMM, 1 + p);
+      L.add(MM_OP_SEND_H, MM_STREAM_COMM, p, 0, root, 0);
+    }
+  }
+  if (rank == root) {
+    for (int p = 0; p < 7; ++p)
+      if (s7_owner(p, world) != root) L.add(MM_OP_RECV_H, MM_STREAM_COMM, p, 0, s7_owner(p, world), 0);
+    L.record(MM_STREAM_COMM, kS7EvGathered);
+    L.wait(MM_STREAM_COMPUTE, kS7EvGathered);
+    L.add(MM_OP_S7_COMBINE, MM_STREAM_COMPUTE, 0, 0, 0, 0);
   }
   return L.ok ? L.n : -1;
 }

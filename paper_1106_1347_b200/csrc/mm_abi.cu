@@ -745,6 +745,83 @@ int mm_dist_step(int method, const mm_dist_op* op, const double* A, const double
   }
 }
 
+}  // extern "C"
+
+// The NCCL executor of a schedule: communication ops in list order on the layer's stream (runs of
+// broadcasts of one panel, or of point-to-point ops, as one NCCL group), compute ops through
+// `step` on the caller's stream, RECORD / WAIT joining the two.
+namespace {
+bool dist_p2p(int op) { return op == MM_OP_SEND_H || op == MM_OP_RECV_H; }
+bool dist_bcast(int op) { return op == MM_OP_BCAST || op == MM_OP_BCAST_A; }
+bool dist_same_group(const mm_dist_op& a, const mm_dist_op& b) {
+  return (dist_bcast(a.op) && dist_bcast(b.op) && a.index == b.index) || (dist_p2p(a.op) && dist_p2p(b.op));
+}
+
+template <class Step>
+int run_dist_ops(const mm_dist_op* ops, int n, double* A, int64_t P, double* B, int64_t M, double* ws,
+                 int64_t hslot, int32_t root, cudaStream_t st, Step step) {
+  mmk::DistState& ds = mmk::dist_state();
+  mmk::NcclApi* api = mmk::nccl_api();
+  cudaStream_t cs = ds.comm_stream;
+  cudaError_t e = cudaEventRecord(ds.start_ev, st);  // buffers may be rewritten once prior work on st is done
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ds.start_ev, 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  bool grouped = false;
+  for (int k = 0; k < n; ++k) {
+    const mm_dist_op& o = ops[k];
+    cudaStream_t os = o.stream == MM_STREAM_COMM ? cs : st;
+    if (dist_bcast(o.op) || dist_p2p(o.op)) {
+      const bool more = k + 1 < n && dist_same_group(o, ops[k + 1]);
+      if (more && !grouped) {
+        if (api->GroupStart() != ncclSuccess) return MM_ERR_NCCL;
+        grouped = true;
+      }
+      ncclResult_t r;
+      if (o.op == MM_OP_BCAST) {
+        r = api->Broadcast(B + o.lo * M, B + o.lo * M, size_t(o.hi - o.lo) * size_t(M), ncclFloat64, root, ds.comm, cs);
+      } else if (o.op == MM_OP_BCAST_A) {
+        r = A ? api->Broadcast(A + o.lo * P, A + o.lo * P, size_t(o.hi - o.lo) * size_t(P), ncclFloat64, root, ds.comm,
+                               cs)
+              : ncclInvalidArgument;
+      } else if (o.op == MM_OP_SEND_H) {
+        r = api->Send(ws + o.index * hslot, size_t(hslot), ncclFloat64, int(o.lo), ds.comm, cs);
+      } else {
+        r = api->Recv(ws + o.index * hslot, size_t(hslot), ncclFloat64, int(o.lo), ds.comm, cs);
+      }
+      if (r != ncclSuccess) {
+        if (grouped) api->GroupEnd();  // leave no NCCL group open behind the error
+        return MM_ERR_NCCL;
+      }
+      if (grouped && !more) {
+        if (api->GroupEnd() != ncclSuccess) return MM_ERR_NCCL;
+        grouped = false;
+      }
+      continue;
+    }
+    switch (o.op) {
+      case MM_OP_ALLREDUCE_NORMS:
+        if (api->AllReduce(ws, ws, 2, ncclFloat64, ncclMax, ds.comm, cs) != ncclSuccess) return MM_ERR_NCCL;
+        break;
+      case MM_OP_RECORD:
+        if ((e = cudaEventRecord(ds.panel_ev[o.index], os)) != cudaSuccess) return cuda_status(e);
+        break;
+      case MM_OP_WAIT:
+        if ((e = cudaStreamWaitEvent(os, ds.panel_ev[o.index], 0)) != cudaSuccess) return cuda_status(e);
+        break;
+      default: {
+        const int rc = step(o);
+        if (rc) return rc;
+      }
+    }
+  }
+  // the caller's stream continues after every communication op of the product
+  if ((e = cudaEventRecord(ds.end_ev, cs)) == cudaSuccess) e = cudaStreamWaitEvent(st, ds.end_ev, 0);
+  return cuda_status(e);
+}
+}  // namespace
+
+extern "C" {
+
 int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, int64_t N_local, int64_t P,
                  int64_t M, int32_t root, int32_t levels, int32_t panels, void* workspace, size_t ws_bytes,
                  void* stream) {
@@ -761,53 +838,144 @@ int mm_dist_gemm(int method, const double* A_shard, double* B, double* C_shard, 
   static thread_local mm_dist_op ops[1024];
   const int n = mmk::build_dist_schedule(method, P, M, levels, panels, ops, 1024);
   if (n < 0) return MM_ERR_ARG;
-  mmk::NcclApi* api = mmk::nccl_api();
-  cudaStream_t st = S(stream), cs = ds.comm_stream;
-  cudaError_t e = cudaEventRecord(ds.start_ev, st);  // B may be rewritten once prior work on st is done
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ds.start_ev, 0);
-  if (e != cudaSuccess) return cuda_status(e);
-  bool grouped = false;  // the broadcasts of one panel (Strassen: 2^span row ranges) are one NCCL group
-  for (int k = 0; k < n; ++k) {
-    const mm_dist_op& o = ops[k];
-    cudaStream_t os = o.stream == MM_STREAM_COMM ? cs : st;
-    switch (o.op) {
-      case MM_OP_BCAST: {
-        const bool more = k + 1 < n && ops[k + 1].op == MM_OP_BCAST && ops[k + 1].index == o.index;
-        if (more && !grouped) {
-          if (api->GroupStart() != ncclSuccess) return MM_ERR_NCCL;
-          grouped = true;
-        }
-        double* Bp = B + o.lo * M;
-        if (api->Broadcast(Bp, Bp, size_t(o.hi - o.lo) * size_t(M), ncclFloat64, root, ds.comm, cs) != ncclSuccess) {
-          if (grouped) api->GroupEnd();  // leave no NCCL group open behind the error
-          return MM_ERR_NCCL;
-        }
-        if (grouped && !more) {
-          if (api->GroupEnd() != ncclSuccess) return MM_ERR_NCCL;
-          grouped = false;
-        }
-        break;
+  return run_dist_ops(ops, n, nullptr, P, B, M, static_cast<double*>(workspace), 0, root, S(stream),
+                      [&](const mm_dist_op& o) {
+                        return mm_dist_step(method, &o, A_shard, B, C_shard, N_local, P, M, levels,
+                                            ds.rank == root ? 1 : 0, workspace, ws_bytes, stream);
+                      });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- the alternative partition (S7)
+namespace {
+struct S7Layout {
+  mmk::StrassenPlan pl, sub;
+  int64_t h2, p2, m2, hslot;     // level-1 node dims, doubles per H slot
+  size_t offL, offR, offSub, total;
+};
+
+bool s7_layout(int method, int64_t N, int64_t P, int64_t M, int32_t levels, S7Layout* o) {
+  if (method != MM_STRASSEN && method != MM_STRASSEN_WINOGRAD) return false;
+  if (levels < 1 || N < 1 || P < 1 || M < 1 || !mul_ok(N, P) || !mul_ok(P, M) || !mul_ok(N, M)) return false;
+  if (!mmk::make_strassen_plan(N, P, M, levels, &o->pl)) return false;
+  o->h2 = o->pl.Np / 2;
+  o->p2 = o->pl.Pp / 2;
+  o->m2 = o->pl.Mp / 2;
+  // the level-1 node recursed on with levels - 1 levels: its plan pads nothing (R10)
+  if (!mmk::make_strassen_plan(o->h2, o->p2, o->m2, levels - 1, &o->sub)) return false;
+  if (o->sub.Np != o->h2 || o->sub.Pp != o->p2 || o->sub.Mp != o->m2) return false;
+  o->hslot = o->h2 * o->m2;
+  o->offL = mmk::align256(size_t(7) * size_t(o->hslot) * 8);
+  o->offR = mmk::align256(o->offL + size_t(o->h2) * size_t(o->p2) * 8);
+  o->offSub = mmk::align256(o->offR + size_t(o->p2) * size_t(o->m2) * 8);
+  o->total = o->offSub + o->sub.total;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+size_t mm_s7_workspace_size(int method, int64_t N, int64_t P, int64_t M, int32_t levels) {
+  S7Layout l;
+  return s7_layout(method, N, P, M, levels, &l) ? l.total : 0;
+}
+
+int mm_s7_schedule(int method, int64_t N, int64_t P, int64_t M, int32_t levels, int32_t world, int32_t rank,
+                   int32_t root, mm_dist_op* ops, int32_t cap) {
+  const int n = mmk::build_s7_schedule(method, N, P, M, levels, world, rank, root, ops, cap);
+  return n < 0 ? MM_ERR_ARG : n;
+}
+
+int mm_s7_step(int method, const mm_dist_op* op, const double* A, const double* B, double* C, int64_t N, int64_t P,
+               int64_t M, int32_t levels, void* workspace, size_t ws_bytes, void* stream) {
+  S7Layout l;
+  if (!op || !A || !B || !s7_layout(method, N, P, M, levels, &l)) return MM_ERR_ARG;
+  if (!workspace || ws_bytes < l.total) return MM_ERR_WORKSPACE;
+  if (overlaps(workspace, int64_t(l.total / 8), A, N * P) || overlaps(workspace, int64_t(l.total / 8), B, P * M))
+    return MM_ERR_ALIAS;
+  int sms = 148;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  mmk::NvtxRange nvtx("mm_s7_step");
+  cudaStream_t st = S(stream);
+  char* ws = static_cast<char*>(workspace);
+  double* Hs = reinterpret_cast<double*>(ws);
+  double* L = reinterpret_cast<double*>(ws + l.offL);
+  double* R = reinterpret_cast<double*>(ws + l.offR);
+  const bool naiv = method == MM_STRASSEN;
+  const int p = op->index;
+  switch (op->op) {
+    case MM_OP_S7_FORM: {  // child p of the zero-embedded level-0 quadrants, both sides
+      if (p < 0 || p > 6) return MM_ERR_ARG;
+      for (int side = 0; side < 2; ++side) {
+        mmk::FormArgs fa;
+        fa.src = side == 0 ? A : B;
+        fa.src_pitch = side == 0 ? P : M;
+        fa.src_stride = 0;
+        fa.rows_valid = side == 0 ? N : P;
+        fa.cols_valid = side == 0 ? P : M;
+        fa.dst = side == 0 ? L : R;
+        fa.h_rows = side == 0 ? l.h2 : l.p2;
+        fa.h_cols = side == 0 ? l.p2 : l.m2;
+        fa.cnt = 1;
+        fa.u0 = 0;
+        fa.u1 = fa.h_rows;
+        const int v = mmk::pick_vec(fa.src, fa.dst, fa.src_pitch, fa.src_stride, fa.h_cols);
+        const cudaError_t e = naiv ? mmk::launch_form_child<mmk::SV_NAIV>(side, fa, p, v, sms, st)
+                                   : mmk::launch_form_child<mmk::SV_WINOGRAD>(side, fa, p, v, sms, st);
+        if (e != cudaSuccess) return cuda_status(e);
       }
-      case MM_OP_ALLREDUCE_NORMS:
-        if (api->AllReduce(workspace, workspace, 2, ncclFloat64, ncclMax, ds.comm, cs) != ncclSuccess)
-          return MM_ERR_NCCL;
-        break;
-      case MM_OP_RECORD:
-        if ((e = cudaEventRecord(ds.panel_ev[o.index], os)) != cudaSuccess) return cuda_status(e);
-        break;
-      case MM_OP_WAIT:
-        if ((e = cudaStreamWaitEvent(os, ds.panel_ev[o.index], 0)) != cudaSuccess) return cuda_status(e);
-        break;
-      default: {
-        const int rc = mm_dist_step(method, &o, A_shard, B, C_shard, N_local, P, M, levels, ds.rank == root ? 1 : 0,
-                                    workspace, ws_bytes, stream);
-        if (rc) return rc;
-      }
+      return MM_OK;
     }
+    case MM_OP_S7_PRODUCT: {  // H_{p+1} with the remaining levels - 1 levels (the one-GPU recursion)
+      if (p < 0 || p > 6) return MM_ERR_ARG;
+      double* H = Hs + p * l.hslot;
+      char* sw = ws + l.offSub;
+      return cuda_status(naiv ? mmk::run_strassen<mmk::SV_NAIV>(L, R, H, l.h2, l.p2, l.m2, l.sub, sw, sms, st)
+                              : mmk::run_strassen<mmk::SV_WINOGRAD>(L, R, H, l.h2, l.p2, l.m2, l.sub, sw, sms, st));
+    }
+    case MM_OP_S7_COMBINE: {  // the level-0 combination into C, dropping the padding
+      if (!C) return MM_ERR_ARG;
+      if (overlaps(C, N * M, A, N * P) || overlaps(C, N * M, B, P * M) ||
+          overlaps(C, N * M, workspace, int64_t(l.total / 8)))
+        return MM_ERR_ALIAS;
+      mmk::CombineArgs ca;
+      ca.H = Hs;
+      ca.dst = C;
+      ca.dst_pitch = M;
+      ca.dst_stride = 0;
+      ca.rows_valid = N;
+      ca.cols_valid = M;
+      ca.h_rows = l.h2;
+      ca.h_cols = l.m2;
+      ca.cnt = 1;
+      const int v = mmk::pick_vec(ca.dst, ca.H, ca.dst_pitch, ca.dst_stride, ca.h_cols);
+      return cuda_status(naiv ? mmk::launch_combine_level<mmk::SV_NAIV>(ca, v, sms, st)
+                              : mmk::launch_combine_level<mmk::SV_WINOGRAD>(ca, v, sms, st));
+    }
+    default: return MM_ERR_ARG;
   }
-  // the caller's stream continues after every communication op of the product
-  if ((e = cudaEventRecord(ds.end_ev, cs)) == cudaSuccess) e = cudaStreamWaitEvent(st, ds.end_ev, 0);
-  return cuda_status(e);
+}
+
+int mm_dist_strassen7(int method, double* A, double* B, double* C, int64_t N, int64_t P, int64_t M, int32_t root,
+                      int32_t levels, void* workspace, size_t ws_bytes, void* stream) {
+  mmk::NvtxRange nvtx("mm_dist_strassen7");
+  mmk::DistState& ds = mmk::dist_state();
+  S7Layout l;
+  if (!ds.comm || !A || !B || root < 0 || root >= ds.world || !s7_layout(method, N, P, M, levels, &l))
+    return MM_ERR_ARG;
+  if (ds.rank == root && !C) return MM_ERR_ARG;
+  if (!workspace || ws_bytes < l.total) return MM_ERR_WORKSPACE;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != ds.device) return MM_ERR_ARG;
+  mm_dist_op ops[64];
+  const int n = mmk::build_s7_schedule(method, N, P, M, levels, ds.world, ds.rank, root, ops, 64);
+  if (n < 0) return MM_ERR_ARG;
+  return run_dist_ops(ops, n, A, P, B, M, static_cast<double*>(workspace), l.hslot, root, S(stream),
+                      [&](const mm_dist_op& o) {
+                        return mm_s7_step(method, &o, A, B, C, N, P, M, levels, workspace, ws_bytes, stream);
+                      });
 }
 
 int norm_inf(const double* X, int64_t rows, int64_t cols, double* out_device, void* stream) {

@@ -183,6 +183,31 @@ __global__ void __launch_bounds__(256) strassen_form_kernel(FormArgs a, int tprs
   }
 }
 
+// One child of each node (the alternative partition, mm_s7_step MM_OP_S7_FORM): child `child`'s
+// operand alone, form1 -- form7's output `child` with exactly its operations -- into cnt dense
+// nodes of h_rows x h_cols.
+template <int VARIANT, int SIDE, int V>
+__global__ void __launch_bounds__(256) strassen_form_child_kernel(FormArgs a, int child, int tprs) {
+  const int sub = threadIdx.x >> tprs, lt = threadIdx.x & ((1 << tprs) - 1);
+  const int64_t rpb = 256 >> tprs, step = int64_t(V) << tprs;
+  const int64_t child_elems = a.h_rows * a.h_cols;
+  for (int64_t u = a.u0 + int64_t(blockIdx.x) * rpb + sub; u < a.u1; u += int64_t(gridDim.x) * rpb) {
+    const int64_t q = u / a.h_rows, i = u - q * a.h_rows;
+    const double* base = a.src + q * a.src_stride;
+    double* d0 = a.dst + q * child_elems + i * a.h_cols;
+    for (int64_t j = int64_t(lt) * V; j < a.h_cols; j += step) {
+      double x11[V], x12[V], x21[V], x22[V], o[V];
+      ld_quad<V>(a, base, i, j, x11);
+      ld_quad<V>(a, base, i, j + a.h_cols, x12);
+      ld_quad<V>(a, base, i + a.h_rows, j, x21);
+      ld_quad<V>(a, base, i + a.h_rows, j + a.h_cols, x22);
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = form1<VARIANT, SIDE>(child, x11[e], x12[e], x21[e], x22[e]);
+      stv<V>(d0 + j, o);
+    }
+  }
+}
+
 // Two recursion levels in one pass (l -> l + 2): each thread reads the 16 sub-blocks' values of
 // a node at one position, forms its 7 children's 4 quadrant values (form7 per quadrant) and
 // from those the 49 grandchildren -- the same per-element operations and order as two
@@ -585,6 +610,30 @@ cudaError_t launch_form_side(const FormArgs& fa, int v, int sms, cudaStream_t st
   }
   note_launch();
   return cudaGetLastError();
+}
+
+template <int VARIANT, int SIDE>
+cudaError_t launch_form_child_side(const FormArgs& fa, int child, int v, int sms, cudaStream_t st) {
+  const int64_t units = fa.u1 - fa.u0;
+  const int tprs = tpr_shift(fa.h_cols, v);
+  if (v == 4) {
+    constexpr auto k = strassen_form_child_kernel<VARIANT, SIDE, 4>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, child, tprs);
+  } else if (v == 2) {
+    constexpr auto k = strassen_form_child_kernel<VARIANT, SIDE, 2>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, child, tprs);
+  } else {
+    constexpr auto k = strassen_form_child_kernel<VARIANT, SIDE, 1>;
+    k<<<grid_for<k>(units, tprs, sms), 256, 0, st>>>(fa, child, tprs);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int VARIANT>
+cudaError_t launch_form_child(int side, const FormArgs& fa, int child, int v, int sms, cudaStream_t st) {
+  return side == 0 ? launch_form_child_side<VARIANT, 0>(fa, child, v, sms, st)
+                   : launch_form_child_side<VARIANT, 1>(fa, child, v, sms, st);
 }
 
 template <int VARIANT>

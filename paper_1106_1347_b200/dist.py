@@ -33,11 +33,13 @@ import torch.distributed as dist
 OP_BCAST, OP_ALLREDUCE_NORMS, OP_RECORD, OP_WAIT = 1, 2, 3, 4
 OP_NORMS, OP_PANEL, OP_YZ, OP_SCALE_A, OP_SCALE_B = 5, 6, 7, 8, 9
 OP_FORM_A, OP_FORM_B, OP_FORM_B_REST, OP_LEAF_COMBINE, OP_FULL = 10, 11, 12, 13, 14
+OP_BCAST_A, OP_S7_FORM, OP_S7_PRODUCT, OP_SEND_H, OP_RECV_H, OP_S7_COMBINE = 15, 16, 17, 18, 19, 20
 STREAM_COMPUTE, STREAM_COMM = 0, 1
 OP_NAMES = {OP_BCAST: "bcast", OP_ALLREDUCE_NORMS: "allreduce_norms", OP_RECORD: "record", OP_WAIT: "wait",
             OP_NORMS: "norms", OP_PANEL: "panel", OP_YZ: "yz", OP_SCALE_A: "scale_a", OP_SCALE_B: "scale_b",
             OP_FORM_A: "form_a", OP_FORM_B: "form_b", OP_FORM_B_REST: "form_b_rest",
-            OP_LEAF_COMBINE: "leaf_combine", OP_FULL: "full"}
+            OP_LEAF_COMBINE: "leaf_combine", OP_FULL: "full", OP_BCAST_A: "bcast_a", OP_S7_FORM: "s7_form",
+            OP_S7_PRODUCT: "s7_product", OP_SEND_H: "send_h", OP_RECV_H: "recv_h", OP_S7_COMBINE: "s7_combine"}
 EX_ACCUMULATE, EX_KEEP_STATE, EX_FUSED = 1, 2, 4
 
 
@@ -166,6 +168,104 @@ def dist_gemm(method: str, A_local: torch.Tensor, B: torch.Tensor, *, out: Optio
     return out
 
 
+# ---- the alternative partition (include/mm.h mm_s7_*): Strassen's seven
+# top-level products H_1..H_7 (PAPER.md:270-277 / 299-306) spread over the ranks, product p on
+# rank p % world; A and B broadcast from the root, every H sent to the root, which combines (level 0).
+def s7_schedule(method: str, N: int, P: int, M: int, levels: int, world: int, rank: int, root: int = 0):
+    """The op list of `rank` (mm_s7_schedule; host only)."""
+    import paper_1106_1347_b200 as mm
+
+    ops = (DistOp * 64)()
+    n = mm.lib().mm_s7_schedule(mm.METHODS[method], N, P, M, levels, world, rank, root, ops, 64)
+    mm._check(n if n < 0 else 0, "mm_s7_schedule")
+    return [ops[i] for i in range(n)]
+
+
+def s7_workspace_bytes(method: str, N: int, P: int, M: int, levels: int) -> int:
+    import paper_1106_1347_b200 as mm
+
+    return int(mm.lib().mm_s7_workspace_size(mm.METHODS[method], N, P, M, levels))
+
+
+def s7_h_slot(ws: torch.Tensor, p: int, N: int, P: int, M: int, levels: int) -> torch.Tensor:
+    """View of H slot p (dense (Np/2) x (Mp/2) float64) of an mm_s7 workspace (layout: include/mm.h)."""
+    import paper_1106_1347_b200 as mm
+
+    _, Np, _, Mp = mm.strassen_plan(N, P, M, levels)
+    h = (Np // 2) * (Mp // 2)
+    return ws[p * h * 8:(p + 1) * h * 8].view(torch.float64).view(Np // 2, Mp // 2)
+
+
+def s7_gpu_step(op: DistOp, ctx: dict) -> None:
+    """Run one compute op of an mm_s7 schedule through mm_s7_step on the current stream."""
+    import paper_1106_1347_b200 as mm
+
+    A, B, C, ws = ctx["A"], ctx["B"], ctx.get("out"), ctx["ws"]
+    N, P = A.shape
+    M = B.shape[1]
+    with torch.cuda.device(B.device):
+        rc = mm.lib().mm_s7_step(mm.METHODS[ctx["method"]], ctypes.byref(op), A.data_ptr(), B.data_ptr(),
+                                 C.data_ptr() if C is not None else None, N, P, M, ctx["levels"], ws.data_ptr(),
+                                 ws.numel(), torch.cuda.current_stream(B.device).cuda_stream)
+    mm._check(rc, f"mm_s7_step({OP_NAMES.get(op.op, op.op)})")
+
+
+def strassen7(method: str, A: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None, root: int = 0,
+              group=None, levels: int = 2, step: Optional[Callable] = None, ctx: Optional[dict] = None,
+              slot: Optional[Callable] = None) -> Optional[torch.Tensor]:
+    """C = A B with Strassen's seven top-level products on the ranks, executing mm_s7_schedule over
+    torch.distributed.  A (N x P) and B (P x M) allocated on every rank; the root's content is
+    broadcast into them.  Returns C on the root (bitwise the one-GPU strassen / strassen_winograd
+    product with the same levels), None elsewhere.  step(op, ctx) runs a compute op (default
+    mm_s7_step on the GPU); slot(ctx, p) gives the tensor H slot p lives in (default: its view of
+    the workspace) -- the CPU tests inject both."""
+    N, P = A.shape
+    M = B.shape[1]
+    if B.shape[0] != P:
+        raise ValueError("inner dimensions differ")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    is_root = rank == root
+    if out is None and is_root:
+        out = torch.empty((N, M), dtype=B.dtype, device=B.device)
+    ctx = dict(ctx or {})
+    ctx.update(method=method, A=A, B=B, out=out if is_root else None, levels=levels, is_root=is_root)
+    if step is None:
+        step = s7_gpu_step
+        nbytes = s7_workspace_bytes(method, N, P, M, levels)
+        if nbytes == 0:
+            raise ValueError("strassen7: method must be strassen / strassen_winograd with levels >= 1")
+        ctx["ws"] = torch.empty(nbytes, dtype=torch.uint8, device=B.device)
+    if slot is None:
+        def slot(c, p):
+            return s7_h_slot(c["ws"], p, N, P, M, levels)
+    pending, events = [], {}
+    for op in s7_schedule(method, N, P, M, levels, world, rank, root):
+        if op.op == OP_BCAST_A:
+            pending.append(dist.broadcast(A[op.lo:op.hi], src=root, group=group, async_op=True))
+        elif op.op == OP_BCAST:
+            pending.append(dist.broadcast(B[op.lo:op.hi], src=root, group=group, async_op=True))
+        elif op.op == OP_SEND_H:
+            pending.append(dist.isend(slot(ctx, op.index), dst=int(op.lo), group=group))
+        elif op.op == OP_RECV_H:
+            pending.append(dist.irecv(slot(ctx, op.index), src=int(op.lo), group=group))
+        elif op.op == OP_RECORD:
+            if op.stream == STREAM_COMM:
+                events[op.index] = pending
+                pending = []
+        elif op.op == OP_WAIT:
+            if op.stream == STREAM_COMPUTE:
+                for w in events.pop(op.index, []):
+                    w.wait()
+        else:
+            step(op, ctx)
+    for w in pending:
+        w.wait()
+    for ws_ in events.values():
+        for w in ws_:
+            w.wait()
+    return out if is_root else None
+
+
 class NativeComm:
     """The C ABI's own multi-GPU layer (mm_dist_*: NCCL driven from libmm_b200.so, the same schedule
     on the library's streams).  torch.distributed only bootstraps it: rank 0's 128-byte NCCL id
@@ -218,6 +318,32 @@ class NativeComm:
                                       out.data_ptr() if N else None, N, P, M, root, levels, panels, ws_ptr, nbytes,
                                       s.cuda_stream), f"mm_dist_gemm({method})")
         return out
+
+    def strassen7(self, method: str, A: torch.Tensor, B: torch.Tensor, *, out: Optional[torch.Tensor] = None,
+                  root: int = 0, levels: int = 2, stream=None) -> Optional[torch.Tensor]:
+        """The alternative partition through mm_dist_strassen7 (A, B on every rank, broadcast in place);
+        C on the root."""
+        mm = self.mm
+        N, P = A.shape
+        M = B.shape[1]
+        for t in (A, B):
+            if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("A and B must be contiguous float64 CUDA tensors")
+        if B.shape[0] != P:
+            raise ValueError("inner dimensions differ")
+        if out is None and self.rank == root:
+            out = torch.empty((N, M), dtype=torch.float64, device=B.device)
+        mid = mm.METHODS[method]
+        nbytes = int(self.L.mm_s7_workspace_size(mid, N, P, M, levels))
+        if nbytes == 0:
+            raise ValueError("strassen7: method must be strassen / strassen_winograd with levels >= 1")
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=B.device)
+        s = stream if stream is not None else torch.cuda.current_stream(B.device)
+        mm._check(self.L.mm_dist_strassen7(mid, A.data_ptr(), B.data_ptr(), out.data_ptr() if out is not None else None,
+                                           N, P, M, root, levels, self._ws.data_ptr(), nbytes, s.cuda_stream),
+                  f"mm_dist_strassen7({method})")
+        return out if self.rank == root else None
 
     def close(self):
         if self.L is not None:

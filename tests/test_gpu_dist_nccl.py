@@ -67,6 +67,20 @@ SCRIPT = textwrap.dedent(r"""
     C0 = comm.gemm("winograd_scaled", dA[:0], hB.clone())
     torch.cuda.synchronize()
     assert C0.shape == (0, hB.shape[1])
+    # the alternative partition (Strassen's seven products on the ranks): all seven on this rank,
+    # through the torch.distributed driver and through mm_dist_strassen7; padded shapes included
+    from paper_1106_1347_b200.dist import strassen7
+    for (n, p_, m_) in ((700, 1024, 520), (300, 1001, 260)):
+        X, Y = workload.custom(n, p_, m_, seed=n + p_)
+        dX, dY = torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev)
+        for m in ("strassen", "strassen_winograd"):
+            for lv in (1, 2, 3):
+                ref = getattr(mm, m)(dX, dY, levels=lv)
+                C = strassen7(m, dX.clone(), dY.clone(), levels=lv)
+                C2 = comm.strassen7(m, dX.clone(), dY.clone(), levels=lv)
+                torch.cuda.synchronize()
+                assert torch.equal(C, ref), ("s7 torch", m, lv, n)
+                assert torch.equal(C2, ref), ("s7 native", m, lv, n)
     comm.close()
     dist.destroy_process_group()
     print("nccl world-1 ok")

@@ -10,6 +10,12 @@ waits for panel i starts at max(end of the previous op, arrival of panel i).  T_
 end of the last op; E_g = T_1 / (g T_g) with T_1 the one-GPU call of the whole problem.
 
     python tools/shard_model.py [--config c4] [--methods ...] [--levels 3] [--panels 8] [--out f.jsonl]
+
+--s7 models the alternative partition instead (include/mm.h mm_s7_*: Strassen's seven top-level
+products on the ranks): every product's S7_FORM + S7_PRODUCT and the root's S7_COMBINE timed on
+one GPU; A and B broadcast at the link rate before any compute, each non-root H (8 (Np/2)(Mp/2)
+bytes) sent once its product ends, the root's inbound link receiving them one after another, the
+combination after the last one.
 """
 from __future__ import annotations
 
@@ -81,6 +87,67 @@ def model(ops, op_ms, M, link_gbs, allreduce_us=25.0):
     return max(t_comp, t_comm), bcast_ms
 
 
+def s7_rows(a, cfg, A, B, T1):
+    """Modelled T_g of the seven-products partition for the Strassen methods (see the docstring)."""
+    N, P, M = cfg.N, cfg.P, cfg.M
+    rows = []
+    for m in (x for x in a.methods.split(",") if x.startswith("strassen")):
+        nb = d.s7_workspace_bytes(m, N, P, M, a.levels)
+        ws = torch.zeros(nb, dtype=torch.uint8, device=B.device)
+        C = torch.empty((N, M), dtype=torch.float64, device=B.device)
+        ctx = dict(method=m, A=A, B=B, out=C, levels=a.levels, ws=ws)
+        form, prod = [0.0] * 7, [0.0] * 7
+        comb = 0.0
+        for r in range(a.reps + 1):
+            evs = []
+            for p in range(7):
+                for kind in (d.OP_S7_FORM, d.OP_S7_PRODUCT):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    d.s7_gpu_step(d.DistOp(kind, 0, p, 0, 0, 0), ctx)
+                    e1.record()
+                    evs.append((kind, p, e0, e1))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            d.s7_gpu_step(d.DistOp(d.OP_S7_COMBINE, 0, 0, 0, 0, 0), ctx)
+            e1.record()
+            torch.cuda.synchronize()
+            if r:  # mean over the timed repetitions
+                for kind, p, x0, x1 in evs:
+                    (form if kind == d.OP_S7_FORM else prod)[p] += x0.elapsed_time(x1) / a.reps
+                comb += e0.elapsed_time(e1) / a.reps
+        ref = getattr(mm, m)(A, B, levels=a.levels)
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref), m  # all seven products on one rank: the one-GPU product
+        _, Np, _, Mp = mm.strassen_plan(N, P, M, a.levels)
+        bw = a.link_gbs * 1e9
+        h_ms = 8.0 * (Np // 2) * (Mp // 2) / bw * 1e3
+        in_ms = 8.0 * (N * P + P * M) / bw * 1e3
+        for g in [int(x) for x in a.gpus.split(",")] + [7]:
+            done = {}
+            in_g = in_ms if g > 1 else 0.0  # one GPU: nothing to broadcast
+            for r in range(g):
+                t = in_g
+                for p in range(7):
+                    if p % g == r:
+                        t += form[p] + prod[p]
+                        done[p] = t
+            root_compute = max([done[p] for p in range(7) if p % g == 0] + [in_g])
+            link = 0.0
+            for p in sorted((p for p in range(7) if p % g != 0), key=lambda p: done[p]):
+                link = max(link, done[p]) + h_ms
+            t = max(root_compute, link) + comb
+            rows.append({"config": a.config, "method": m, "partition": "s7", "g": g, "levels": a.levels,
+                         "inputs_bcast_ms": round(in_ms, 3), "h_send_ms": round(h_ms, 3),
+                         "form_ms": [round(x, 4) for x in form], "product_ms": [round(x, 3) for x in prod],
+                         "combine_ms": round(comb, 4), "modelled_T_g_ms": round(t, 3), "T_1_ms": round(T1[m], 3),
+                         "E_g": round(T1[m] / (g * t), 4), "link_gbs": a.link_gbs})
+            print(json.dumps(rows[-1]), flush=True)
+        del ws, C
+        torch.cuda.empty_cache()
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
@@ -91,6 +158,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--link-gbs", type=float, default=770.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--s7", action="store_true", help="model the seven-products partition of the Strassen methods")
     a = ap.parse_args()
     cfg = workload.CONFIGS[a.config]
     N, P, M = cfg.N, cfg.P, cfg.M
@@ -99,6 +167,28 @@ def main():
     B = torch.from_numpy(workload.matrix(cfg, 1)).to(dev)
     methods = a.methods.split(",")
     gs = [int(x) for x in a.gpus.split(",")]
+    if a.s7:
+        T1 = {}
+        for m in (x for x in methods if x.startswith("strassen")):
+            out = torch.empty((N, M), dtype=torch.float64, device=dev)
+            getattr(mm, m)(A, B, out=out, levels=a.levels)
+            ts = []
+            for _ in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                getattr(mm, m)(A, B, out=out, levels=a.levels)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            T1[m] = statistics.median(ts)
+            del out
+        mm.release_workspace()
+        rows = s7_rows(a, cfg, A, B, T1)
+        if a.out:
+            with open(a.out, "w") as fh:
+                for r in rows:
+                    fh.write(json.dumps(r) + "\n")
+        return
     rows, T1, Tg = [], {}, {g: 0.0 for g in gs}
     for m in methods:
         kw = {"levels": a.levels} if m.startswith("strassen") else {}
