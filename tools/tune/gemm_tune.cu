@@ -125,7 +125,8 @@ int main(int argc, char** argv) {
     run_rect<GemmCfg<64, 64, 2, 2, 4, 4>, false>("cpasync_64x64_2048_P2047", A2, B2, C2, 2048, 2047, 2048, 10);
     return 0;
   }
-  int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
+  const bool raster = argc > 1 && argv[1][0] == 'g';  // production K1 with GROUP_M varied (L2 reuse / DRAM bytes)
+  int64_t n = argc > 1 && !raster ? atoll(argv[1]) : 8192;
   int reps = argc > 2 ? atoi(argv[2]) : 3;
   double *A, *B, *C, *R;
   unsigned long long* bad;
@@ -137,6 +138,24 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(A, n * n, 1);
   fill<<<1024, 256>>>(B, n * n, 2);
   run<GemmCfg<64, 64, 2, 2, 2, 3, 32>, true>("tma_64x64_s2_3cta_bk32", A, B, R, nullptr, n, reps, bad);
+  if (n == 1024 && argc > 3) {  // "1024 <reps> s": small-grid TMA configurations at 1024^3 (r02)
+    run<GemmCfg<64, 32, 2, 1, 4, 6, 16>, true>("tma_64x32_w2x1_s4_6cta_bk16", A, B, C, R, n, reps, bad);
+    run<GemmCfg<32, 32, 1, 1, 2, 8, 32>, true>("tma_32x32_w1_s2_8cta_bk32", A, B, C, R, n, reps, bad);
+    run<GemmCfg<32, 32, 1, 1, 3, 8, 32>, true>("tma_32x32_w1_s3_8cta_bk32", A, B, C, R, n, reps, bad);
+    run<GemmCfg<32, 32, 1, 1, 4, 8, 16>, true>("tma_32x32_w1_s4_8cta_bk16", A, B, C, R, n, reps, bad);
+    run<GemmCfg<32, 64, 1, 2, 3, 6, 32>, true>("tma_32x64_w1x2_s3_6cta_bk32", A, B, C, R, n, reps, bad);
+    run<GemmCfg<64, 32, 2, 1, 3, 6, 32>, true>("tma_64x32_w2x1_s3_6cta_bk32", A, B, C, R, n, reps, bad);
+    run<GemmCfg<32, 32, 1, 1, 2, 12, 32>, true>("tma_32x32_w1_s2_12cta_bk32", A, B, C, R, n, reps, bad);
+    return 0;
+  }
+  if (raster) {
+    run<GemmCfg<64, 64, 2, 2, 2, 3, 32, 4>, true>("tma_64x64_group4", A, B, C, R, n, reps, bad);
+    run<GemmCfg<64, 64, 2, 2, 2, 3, 32, 8>, true>("tma_64x64_group8", A, B, C, R, n, reps, bad);
+    run<GemmCfg<64, 64, 2, 2, 2, 3, 32, 16>, true>("tma_64x64_group16", A, B, C, R, n, reps, bad);
+    run<GemmCfg<64, 64, 2, 2, 2, 3, 32, 24>, true>("tma_64x64_group24", A, B, C, R, n, reps, bad);
+    run<GemmCfg<64, 64, 2, 2, 2, 3, 32, 32>, true>("tma_64x64_group32", A, B, C, R, n, reps, bad);
+    return 0;
+  }
   run<GemmCfg<64, 64, 2, 2, 2, 2, 32>, true>("tma_64x64_s2_2cta_bk32", A, B, C, R, n, reps, bad);
   run<GemmCfg<64, 64, 2, 2, 3, 2, 32>, true>("tma_64x64_s3_2cta_bk32", A, B, C, R, n, reps, bad);
   run<GemmCfg<128, 64, 4, 2, 2, 2, 32>, true>("tma_128x64_w4x2_s2_2cta_bk32", A, B, C, R, n, reps, bad);

@@ -172,6 +172,22 @@ int main(int argc, char** argv) {
     kahan<SimtCfg<32, 32, 2, 4, 3, 4>>("kahan_32x32_t2x4_s3_4cta", c, true);
     kahan<SimtCfg<32, 32, 2, 4, 4, 6>>("kahan_32x32_t2x4_s4_6cta", c, false);
     kahan<SimtCfg<32, 64, 2, 8, 3, 4>>("kahan_32x64_t2x8_s3_4cta", c, false);
+    if (argv[1][1] == 't') {  // "st": TMA-fed small-grid configurations at 1024^3 (r02)
+      wino<SimtCfg<64, 64, 4, 8, 3, 2>>("wino_64x64_t4x8_s3_2cta", c, true);
+      wino_tma<SimtCfg<64, 64, 4, 8, 2, 2, 32>>("wino_tma_64x64_t4x8_s2_2cta_bk32", c);
+      wino_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("wino_tma_64x64_t4x8_s3_2cta_bk32", c);
+      wino_tma<SimtCfg<64, 64, 4, 8, 4, 2, 16>>("wino_tma_64x64_t4x8_s4_2cta_bk16", c);
+      wino_tma<SimtCfg<64, 64, 4, 8, 2, 3, 32>>("wino_tma_64x64_t4x8_s2_3cta_bk32", c);
+      wino_tma<SimtCfg<32, 64, 2, 8, 3, 4, 32>>("wino_tma_32x64_t2x8_s3_4cta_bk32", c);
+      wino_tma<SimtCfg<64, 64, 8, 8, 3, 4, 32>>("wino_tma_64x64_t8x8_s3_4cta_bk32", c);
+      wino_tma<SimtCfg<64, 64, 8, 8, 4, 4, 16>>("wino_tma_64x64_t8x8_s4_4cta_bk16", c);
+      kahan<SimtCfg<32, 32, 2, 4, 3, 4>>("kahan_32x32_t2x4_s3_4cta", c, true);
+      kahan_tma<SimtCfg<32, 32, 2, 4, 3, 4, 32>>("kahan_tma_32x32_t2x4_s3_4cta_bk32", c);
+      kahan_tma<SimtCfg<32, 32, 2, 4, 4, 6, 16>>("kahan_tma_32x32_t2x4_s4_6cta_bk16", c);
+      kahan_tma<SimtCfg<32, 64, 2, 8, 3, 4, 32>>("kahan_tma_32x64_t2x8_s3_4cta_bk32", c);
+      kahan_tma<SimtCfg<64, 32, 4, 4, 3, 4, 32>>("kahan_tma_64x32_t4x4_s3_4cta_bk32", c);
+      kahan_tma<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("kahan_tma_64x64_t4x8_s3_2cta_bk32", c);
+    }
     return 0;
   }
   if (kahan_only) {  // K2 configurations only
