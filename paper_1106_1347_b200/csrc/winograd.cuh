@@ -40,6 +40,10 @@ using WinogradTma = SimtCfg<128, 64, 8, 8, 2, 2, 32>;
 // ... and a finer tile grid for shapes whose last wave of 128 x 64 tiles is mostly empty (c3: 5.08
 // waves; 96 x 64 at 3 CTAs per SM: 4.55), 2.5% slower per tile at 8192^3 (66.7 vs 65.1 ms)
 using WinogradTma96 = SimtCfg<96, 64, 6, 8, 3, 3, 16>;
+// ... and the small-grid tiles (fewer than two waves of 128 x 64 tiles, e.g. c2 = 1024^3), TMA-fed:
+// 0.177 vs 0.191 ms for the cp.async WinogradSmall at 1024^3, bitwise equal (tools/tune/simt_tune.cu
+// st, profiles/r02/small_tune.md)
+using WinogradTmaSmall = SimtCfg<64, 64, 4, 8, 3, 2, 32>;
 
 // odd P on even-pitch copies (repack.cuh / WinogradScaled's 2^lambda A): the TMA pair kernel with
 // the odd term in its epilogue, on the tile grid that fills its last wave better
@@ -199,6 +203,8 @@ inline cudaError_t launch_winograd_pairs(const double* A, const double* B, doubl
     if (f96 > f128) return launch_winograd_main<Winograd96, FUSED>(A, B, C, y, z, N, P, M, st);
     return launch_winograd_main<WinogradDefault, FUSED>(A, B, C, y, z, N, P, M, st);
   }
+  if (simt_tma_ok(A, B, N, P, M))
+    return launch_winograd_pairs_tma<WinogradTmaSmall, FUSED>(A, B, C, y, z, N, P, M, st);
   return launch_winograd_main<WinogradSmall, FUSED>(A, B, C, y, z, N, P, M, st);
 }
 
