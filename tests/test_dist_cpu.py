@@ -218,13 +218,16 @@ def _run(world, N, P, M, seed):
     return sorted(res, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("shape", [(9, 13, 7), (1, 5, 3), (16, 8, 16), (7, 20, 10), (12, 32, 6)])
-def test_row_sharded_bitwise(shape):
+@pytest.mark.parametrize("world,shape", [(2, (9, 13, 7)), (2, (1, 5, 3)), (2, (16, 8, 16)), (2, (7, 20, 10)),
+                                         (2, (12, 32, 6)), (3, (2, 6, 5)), (4, (11, 10, 9))])
+def test_row_sharded_bitwise(world, shape):
+    """world 3 with N = 2 leaves rank 2 without rows (it still takes part in every collective);
+    world 4 with N = 11 gives shards of 3, 3, 3, 2 rows."""
     import oracle
     import workload
 
     N, P, M = shape
-    res = _run(2, N, P, M, seed=N + P + M)
+    res = _run(world, N, P, M, seed=N + P + M)
     A, B = workload.custom(N, P, M, seed=N + P + M)
     A = A * 1e5
     full = {m: _oracle_full(m, A, B, 0, 0) for m in METHODS if not m.startswith(("winograd_scaled", "strassen"))}
