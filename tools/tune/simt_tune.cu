@@ -205,6 +205,10 @@ int main(int argc, char** argv) {
     wino<SimtCfg<128, 64, 8, 8, 3, 2>>("cpasync_128x64_bk16", c, true);
     wino_tma<SimtCfg<128, 64, 8, 8, 2, 2, 32>>("tma_128x64_s2_2cta_bk32", c);
     wino_tma<SimtCfg<128, 64, 8, 8, 3, 2, 32>>("tma_128x64_s3_2cta_bk32", c);
+    if (argv[1][1] == 'd') {  // "xd": deeper rings of 16-deep k tiles in the same shared memory (r02)
+      wino_tma<SimtCfg<128, 64, 8, 8, 4, 2, 16>>("tma_128x64_s4_2cta_bk16", c);
+      wino_tma<SimtCfg<128, 64, 8, 8, 3, 2, 16>>("tma_128x64_s3_2cta_bk16", c);
+    }
     return 0;
   }
   if (argc > 1 && argv[1][0] == 'y') {  // the production K2 configuration only (unroll variants)
