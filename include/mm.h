@@ -194,8 +194,8 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
  * of A as it lands; a last row-local method returns its product by row blocks of halving height.
  * Every C_host[i] equals the device entry point's result bit for bit.  levels: for the Strassen
  * methods (as mm_strassen).  dev_ws: DEVICE workspace of at least
- * mm_methods_host_workspace_size(methods, n, N, P, M, levels) bytes (device copies of A and B, two
- * product buffers, the largest method workspace).  SYNCHRONOUS: returns once every product has
+ * mm_methods_host_workspace_size(methods, n, N, P, M, levels) bytes (device copies of A and B,
+ * min(n, 3) product buffers, the largest method workspace).  SYNCHRONOUS: returns once every product has
  * landed in host memory.  The library keeps two copy streams per device for these calls.
  * Errors as mm_gemm; MM_ERR_ARG for a NULL C_host[i] or an unknown method id.
  */

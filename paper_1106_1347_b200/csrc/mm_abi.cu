@@ -417,6 +417,12 @@ int mm_gemm(int method, const double* A, const double* B, double* C, int64_t N, 
 }
 
 // ---------------------------------------------------------------- host buffers (the paper's test program)
+// product buffers of mm_methods_host: method i computes into buffer i % 3 once the copy-back of
+// method i - 3 has left it, so every copy-back overlaps at least the two methods after it (with two
+// buffers a copy-back slower than the next method -- c4's 537 MB behind a 22 ms Strassen call on
+// a slow host link -- stalled the third method)
+constexpr int kHostCBuffers = 3;
+
 static size_t host_ws_method(const int* methods, int32_t n, int64_t N, int64_t P, int64_t M, int32_t levels) {
   size_t w = 0;
   for (int i = 0; i < n; ++i) {
@@ -429,7 +435,7 @@ static size_t host_ws_method(const int* methods, int32_t n, int64_t N, int64_t P
 size_t mm_methods_host_workspace_size(const int* methods, int32_t n, int64_t N, int64_t P, int64_t M,
                                       int32_t levels) {
   if (!methods || n < 1 || N < 1 || P < 1 || M < 1 || !mul_ok(N, P) || !mul_ok(P, M) || !mul_ok(N, M)) return 0;
-  const size_t nc = n > 1 ? 2 : 1;
+  const size_t nc = size_t(n < kHostCBuffers ? n : kHostCBuffers);
   return mmk::align256(size_t(N) * size_t(P) * 8) + mmk::align256(size_t(P) * size_t(M) * 8) +
          nc * mmk::align256(size_t(N) * size_t(M) * 8) + host_ws_method(methods, n, N, P, M, levels);
 }
@@ -453,11 +459,12 @@ int mm_methods_host(const int* methods, int32_t n, const double* A_host, const d
   w += mmk::align256(size_t(N) * size_t(P) * 8);
   double* dB = reinterpret_cast<double*>(w);
   w += mmk::align256(size_t(P) * size_t(M) * 8);
-  double* dC[2];
-  dC[0] = reinterpret_cast<double*>(w);
-  w += mmk::align256(size_t(N) * size_t(M) * 8);
-  dC[1] = n > 1 ? reinterpret_cast<double*>(w) : dC[0];
-  if (n > 1) w += mmk::align256(size_t(N) * size_t(M) * 8);
+  const int nc = n < kHostCBuffers ? n : kHostCBuffers;
+  double* dC[kHostCBuffers];
+  for (int k = 0; k < nc; ++k) {
+    dC[k] = reinterpret_cast<double*>(w);
+    w += mmk::align256(size_t(N) * size_t(M) * 8);
+  }
   void* wsm = w;
   const size_t wsm_bytes = host_ws_method(methods, n, N, P, M, levels);
 
@@ -520,11 +527,11 @@ int mm_methods_host(const int* methods, int32_t n, const double* A_host, const d
     }
   }
   cudaEvent_t inputs_done = ready.back();
-  cudaEvent_t buf_free[2] = {nullptr, nullptr};
+  cudaEvent_t buf_free[kHostCBuffers] = {};
   // ---- the methods
   for (int i = 0; i < n; ++i) {
     const int m = methods[i];
-    const int k = i % 2;
+    const int k = i % nc;
     double* C = dC[k];
     if (buf_free[k]) MMH_TRY(cudaStreamWaitEvent(st, buf_free[k], 0));  // its previous product has left
     auto d2h = [&](int64_t lo, int64_t hi) -> cudaError_t {
