@@ -84,6 +84,22 @@ void run_rect(const char* name, const double* A, const double* B, double* C, int
 }
 
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "panel") {  // k-panel launches of the g = 2 / 4 / 8 c4 shards (r02)
+    double *A, *B, *C;
+    cudaMalloc(&A, 4096ll * 1024 * 8);
+    cudaMalloc(&B, 1024ll * 8192 * 8);
+    cudaMalloc(&C, 4096ll * 8192 * 8);
+    fill<<<1024, 256>>>(A, 4096ll * 1024, 1);
+    fill<<<1024, 256>>>(B, 1024ll * 8192, 2);
+    for (int64_t rows : {1024, 2048, 4096}) {
+      run_rect<GemmCfg<64, 64, 2, 2, 2, 3, 32>, true>("tma_64x64_s2_3cta_bk32", A, B, C, rows, 1024, 8192, 20);
+      run_rect<GemmCfg<64, 64, 2, 2, 2, 2, 32>, true>("tma_64x64_s2_2cta_bk32", A, B, C, rows, 1024, 8192, 20);
+      run_rect<GemmCfg<64, 64, 2, 2, 3, 2, 32>, true>("tma_64x64_s3_2cta_bk32", A, B, C, rows, 1024, 8192, 20);
+      run_rect<GemmCfg<64, 32, 2, 1, 4, 6, 16>, true>("tma_64x32_s4_6cta_bk16", A, B, C, rows, 1024, 8192, 20);
+      run_rect<GemmCfg<128, 64, 2, 2, 3, 2, 32>, true>("tma_128x64_s3_2cta_bk32", A, B, C, rows, 1024, 8192, 20);
+    }
+    return 0;
+  }
   if (argc > 1 && std::string(argv[1]) == "c3") {
     double *A, *B, *C;
     cudaMalloc(&A, 4096 * 1002 * 8);

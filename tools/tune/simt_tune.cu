@@ -4,6 +4,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o simt_tune simt_tune.cu
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "../../paper_1106_1347_b200/csrc/kahan.cuh"
 #include "../../paper_1106_1347_b200/csrc/winograd.cuh"
@@ -113,7 +114,142 @@ void rect(const char* kind, const char* name, const double* A, const double* B, 
   fflush(stdout);
 }
 
+// c3 after the odd-P repack (A at the even pitch P + 1 = 1002): TMA-fed K2 / K3 tile variants, each
+// compared bitwise with the first of its kind (r02)
+struct OddCtx {
+  double *A, *B, *C, *R, *y, *z;
+  unsigned long long* bad;
+  bool have_ref = false;
+};
+template <class F>
+void odd_time(const char* kind, const char* name, OddCtx& c, F f) {
+  const int64_t N = 4096, M = 3000;
+  cudaMemset(c.C, 0, N * M * 8);
+  f();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 20; ++r) f();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long nb = 0;
+  if (c.have_ref) {
+    cudaMemset(c.bad, 0, 8);
+    cmp<<<1024, 256>>>(c.C, c.R, N * M, c.bad);
+    cudaMemcpy(&nb, c.bad, 8, cudaMemcpyDeviceToHost);
+  } else {
+    cudaMemcpy(c.R, c.C, N * M * 8, cudaMemcpyDeviceToDevice);
+    c.have_ref = true;
+  }
+  printf("{\"kernel\":\"%s\",\"cfg\":\"%s\",\"N\":4096,\"P\":1001,\"M\":3000,\"ms\":%.4f,\"mismatch\":%llu,"
+         "\"err\":\"%s\"}\n",
+         kind, name, ms / 20, nb, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+template <class CF>
+void odd_wino(const char* name, OddCtx& c) {
+  odd_time("winograd", name, c, [&] {
+    launch_winograd_pairs_tma_odd<CF, false>(c.A, 1002, c.B, 3000, c.C, c.y, c.z, 4096, 1001, 3000, 0);
+  });
+}
+template <class CF>
+void odd_kahan(const char* name, OddCtx& c) {
+  odd_time("kahan", name, c, [&] {
+    launch_kahan_tma_ex<CF, false>(c.A, 1002, c.B, 3000, c.C, nullptr, 4096, 1001, 3000, 0, 0);
+  });
+}
+
+// K3 at the c4 shard heights of the g-GPU row partition (rows x 8192 x 8192), r02
+template <class CF>
+void shard_wino(const char* name, Ctx& c, int64_t rows, bool first) {
+  const int64_t n = c.n;
+  cudaMemset(c.C, 0, rows * n * 8);
+  auto go = [&] { launch_winograd_pairs_tma<CF, false>(c.A, c.B, c.C, c.y, c.z, rows, n, n, 0); };
+  go();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < c.reps; ++r) go();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long nb = 0;
+  if (first) {
+    cudaMemcpy(c.R, c.C, rows * n * 8, cudaMemcpyDeviceToDevice);
+  } else {
+    cudaMemset(c.bad, 0, 8);
+    cmp<<<1024, 256>>>(c.C, c.R, rows * n, c.bad);
+    cudaMemcpy(&nb, c.bad, 8, cudaMemcpyDeviceToHost);
+  }
+  printf("{\"kernel\":\"winograd\",\"cfg\":\"%s\",\"N\":%lld,\"P\":%lld,\"M\":%lld,\"ms\":%.4f,"
+         "\"fp64_op_rate_T\":%.3f,\"mismatch\":%llu,\"err\":\"%s\"}\n",
+         name, (long long)rows, (long long)n, (long long)n, ms / c.reps, 2.0 * rows * n * n / (ms / c.reps) / 1e9, nb,
+         cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'h') {
+    Ctx c;
+    c.n = 8192;
+    c.reps = 10;
+    cudaMalloc(&c.A, c.n * c.n * 8);
+    cudaMalloc(&c.B, c.n * c.n * 8);
+    cudaMalloc(&c.C, c.n * c.n * 8);
+    cudaMalloc(&c.R, c.n * c.n * 8);
+    cudaMalloc(&c.y, c.n * 8);
+    cudaMalloc(&c.z, c.n * 8);
+    cudaMalloc(&c.bad, 8);
+    fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
+    fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
+    cudaMemset(c.y, 0, c.n * 8);
+    cudaMemset(c.z, 0, c.n * 8);
+    std::vector<int64_t> heights = {1024, 2048, 4096};
+    if (argc > 2) heights = {atoll(argv[2])};  // "h 8192": one height
+    for (int64_t rows : heights) {
+      shard_wino<WinogradTma>("tma_128x64_t8x8_s2_2cta_bk32", c, rows, true);
+      shard_wino<SimtCfg<112, 64, 7, 8, 3, 2, 16>>("tma_112x64_t7x8_s3_2cta_bk16", c, rows, false);
+      shard_wino<WinogradTma96>("tma_96x64_t6x8_s3_3cta_bk16", c, rows, false);
+      shard_wino<SimtCfg<112, 64, 7, 8, 2, 2, 32>>("tma_112x64_t7x8_s2_2cta_bk32", c, rows, false);
+      shard_wino<SimtCfg<64, 64, 4, 8, 3, 2, 32>>("tma_64x64_t4x8_s3_2cta_bk32", c, rows, false);
+      shard_wino<SimtCfg<64, 64, 4, 8, 2, 3, 32>>("tma_64x64_t4x8_s2_3cta_bk32", c, rows, false);
+    }
+    return 0;
+  }
+  if (argc > 1 && argv[1][0] == 'o') {
+    OddCtx c;
+    cudaMalloc(&c.A, 4096 * 1002 * 8);
+    cudaMalloc(&c.B, 1001 * 3000 * 8);
+    cudaMalloc(&c.C, 4096 * 3000 * 8);
+    cudaMalloc(&c.R, 4096 * 3000 * 8);
+    cudaMalloc(&c.y, 4096 * 8);
+    cudaMalloc(&c.z, 3000 * 8);
+    cudaMalloc(&c.bad, 8);
+    fill<<<1024, 256>>>(c.A, 4096 * 1002, 1);
+    fill<<<1024, 256>>>(c.B, 1001 * 3000, 2);
+    cudaMemset(c.y, 0, 4096 * 8);
+    cudaMemset(c.z, 0, 3000 * 8);
+    odd_wino<WinogradTma>("wino_tma_128x64_t8x8_s2_2cta_bk32", c);
+    odd_wino<WinogradTma96>("wino_tma_96x64_t6x8_s3_3cta_bk16", c);
+    odd_wino<SimtCfg<112, 64, 7, 8, 2, 2, 32>>("wino_tma_112x64_t7x8_s2_2cta_bk32", c);
+    odd_wino<SimtCfg<112, 64, 7, 8, 3, 2, 16>>("wino_tma_112x64_t7x8_s3_2cta_bk16", c);
+    odd_wino<SimtCfg<64, 64, 4, 8, 3, 3, 32>>("wino_tma_64x64_t4x8_s3_3cta_bk32", c);
+    odd_wino<SimtCfg<80, 64, 5, 8, 2, 3, 32>>("wino_tma_80x64_t5x8_s2_3cta_bk32", c);
+    c.have_ref = false;
+    odd_kahan<KahanTma>("kahan_tma_64x64_t4x8_s3_2cta_bk32", c);
+    odd_kahan<SimtCfg<48, 64, 3, 8, 3, 3, 32>>("kahan_tma_48x64_t3x8_s3_3cta_bk32", c);
+    odd_kahan<SimtCfg<48, 64, 3, 8, 2, 3, 32>>("kahan_tma_48x64_t3x8_s2_3cta_bk32", c);
+    odd_kahan<SimtCfg<32, 64, 2, 8, 3, 4, 32>>("kahan_tma_32x64_t2x8_s3_4cta_bk32", c);
+    odd_kahan<SimtCfg<80, 64, 5, 8, 2, 2, 32>>("kahan_tma_80x64_t5x8_s2_2cta_bk32", c);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'c') {
     double *A, *B, *C, *y, *z;
     cudaMalloc(&A, 4096 * 1002 * 8);
