@@ -31,10 +31,13 @@
 #ifndef MMK_WINO_UNROLL
 #define MMK_WINO_UNROLL 8
 #endif
+#ifndef MMK_WINO_UNROLL_EX
+#define MMK_WINO_UNROLL_EX 4
+#endif
 
 namespace mmk {
 
-constexpr int kWinoUnroll = MMK_WINO_UNROLL, kKahanUnroll = MMK_KAHAN_UNROLL;
+constexpr int kWinoUnroll = MMK_WINO_UNROLL, kWinoUnrollEx = MMK_WINO_UNROLL_EX, kKahanUnroll = MMK_KAHAN_UNROLL;
 
 struct SimtTmaArgs {
   CUtensorMap mapA, mapB;
@@ -273,8 +276,10 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) winograd_tma_kernel(con
     // per pair: B's TN column pairs stay in registers, A's pair of row i is read just before its
     // TN entries (64.70 vs 65.02 ms with all of A's pairs loaded up front; winograd_sched.log)
     // 8 pairs per unrolled body on the 2-CTA tiles: 63.9 vs 64.7 ms at 8192^3 with 2
-    // (tools/tune/simt_tune.cu x, profiles/r02/winograd_unroll.log); the 3-CTA tiles keep 2
-    constexpr int UNR = CF::MINB >= 3 ? 2 : kWinoUnroll;
+    // (tools/tune/simt_tune.cu x, profiles/r02/winograd_unroll.log); the 3-CTA tiles keep 2.  The
+    // k-panel variant (EX) takes 4: the g = 8 c4 shard's four 2048-deep panels 8.19 vs 8.50 ms with
+    // 8, 32.20 vs 32.58 at 4096 rows, equal at 8192 (simt_tune e, profiles/r02/winograd_unroll_ex.jsonl)
+    constexpr int UNR = CF::MINB >= 3 ? 2 : (EX ? kWinoUnrollEx : kWinoUnroll);
 #pragma unroll UNR
     for (int jp = 0; jp < CF::BK / 2; ++jp) {
       double b0[TN], b1[TN];

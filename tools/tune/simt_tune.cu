@@ -195,7 +195,51 @@ void shard_wino(const char* name, Ctx& c, int64_t rows, bool first) {
   fflush(stdout);
 }
 
+// the g = 8 c4 Winograd panel schedule on one GPU: 1024 rows, four 2048-deep k-panels accumulated
+// with mm_winograd_ex's flags (compile with -DMMK_WINO_UNROLL=2 / 8 to compare unrolls), r02
+void panel_wino(Ctx& c, int64_t rows, int np) {
+  const int64_t n = c.n, kp = n / np;
+  auto go = [&] {
+    for (int i = 0; i < np; ++i) {
+      const int f = (i > 0 ? SIMT_EX_ACC : 0) | (i < np - 1 ? SIMT_EX_KEEP : 0);
+      launch_winograd_tma_ex<WinogradTma, false>(c.A + i * kp, n, c.B + i * kp * n, n, c.C, c.y, c.z, rows, kp, n, f,
+                                                 0);
+    }
+  };
+  go();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < c.reps; ++r) go();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("{\"kernel\":\"winograd_panels\",\"unroll\":%d,\"rows\":%lld,\"panels\":%d,\"ms\":%.4f,\"err\":\"%s\"}\n",
+         kWinoUnroll, (long long)rows, np, ms / c.reps, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'e') {
+    Ctx c;
+    c.n = 8192;
+    c.reps = 10;
+    cudaMalloc(&c.A, c.n * c.n * 8);
+    cudaMalloc(&c.B, c.n * c.n * 8);
+    cudaMalloc(&c.C, c.n * c.n * 8);
+    cudaMalloc(&c.y, c.n * 8);
+    cudaMalloc(&c.z, c.n * 8);
+    fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
+    fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
+    cudaMemset(c.y, 0, c.n * 8);
+    cudaMemset(c.z, 0, c.n * 8);
+    for (int64_t rows : {1024, 2048, 4096, 8192}) panel_wino(c, rows, 4);
+    panel_wino(c, 8192, 1);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'h') {
     Ctx c;
     c.n = 8192;
