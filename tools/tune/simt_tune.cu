@@ -222,7 +222,44 @@ void panel_wino(Ctx& c, int64_t rows, int np) {
   fflush(stdout);
 }
 
+void panel_kahan(Ctx& c, double* E, int64_t rows, int np) {
+  const int64_t n = c.n, kp = n / np;
+  auto go = [&] {
+    for (int i = 0; i < np; ++i) {
+      const int f = (i > 0 ? SIMT_EX_ACC : 0) | (i < np - 1 ? SIMT_EX_KEEP : 0);
+      launch_kahan_tma_ex<KahanTma, false>(c.A + i * kp, n, c.B + i * kp * n, n, c.C, E, rows, kp, n, f, 0);
+    }
+  };
+  go();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) go();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("{\"kernel\":\"kahan_panels\",\"unroll\":%d,\"rows\":%lld,\"panels\":%d,\"ms\":%.4f,\"err\":\"%s\"}\n",
+         kKahanUnroll, (long long)rows, np, ms / 3, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'K') {  // the Kahan panel schedule (compile with -DMMK_KAHAN_UNROLL=k)
+    Ctx c;
+    c.n = 8192;
+    double* E;
+    cudaMalloc(&c.A, c.n * c.n * 8);
+    cudaMalloc(&c.B, c.n * c.n * 8);
+    cudaMalloc(&c.C, c.n * c.n * 8);
+    cudaMalloc(&E, c.n * c.n * 8);
+    fill<<<1024, 256>>>(c.A, c.n * c.n, 1);
+    fill<<<1024, 256>>>(c.B, c.n * c.n, 2);
+    for (int64_t rows : {1024, 4096}) panel_kahan(c, E, rows, 4);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'e') {
     Ctx c;
     c.n = 8192;
