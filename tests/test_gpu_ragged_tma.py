@@ -49,3 +49,20 @@ def test_ragged_gemm_big_config_bitwise():
     idx += [(N - 1, j) for j in range(M)] + [(i, M - 1) for i in range(0, N, 7)]
     ref = oracle.entries(oracle.M_FMA, A, B, idx)
     assert np.array_equal(np.array([C[i, j] for i, j in idx]), ref)
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 2), (37, 46, 98), (100, 258, 130), (513, 1000, 514), (1000, 66, 1024)])
+def test_small_grid_tma_winograd_bitwise(shape):
+    """Grids under two waves of 128 x 64 tiles with P, M even and aligned operands take the
+    TMA-fed 64 x 64 small-grid kernel (winograd.cuh WinogradTmaSmall, r02): ragged N and M, a
+    partial last 32-deep k tile, a single-row problem; full products against the oracle, plain,
+    scaled (lambda != 0) and fused."""
+    N, P, M = shape
+    A, B = workload.custom(N, P, M, seed=N + 7 * P + 13 * M)
+    A = A * 1e4
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    assert np.array_equal(mm.winograd(dA, dB).cpu().numpy(), oracle.winograd_original(A, B)), shape
+    C, lam = oracle.winograd_scaled(A, B)
+    assert lam != 0
+    assert np.array_equal(mm.winograd_scaled(dA, dB).cpu().numpy(), C), shape
+    assert np.array_equal(mm.winograd_fused(dA, dB).cpu().numpy(), oracle.winograd_fused(A, B)), shape
